@@ -1,0 +1,259 @@
+"""ORACLE (test infrastructure only) -- plain, slow, obviously-correct CPU float64
+implementation of the Gram-based SVD hot path of Li, Kluger & Tygert,
+"Algorithms for distributed computation of PCA and SVD" (arXiv 1612.08709).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` legs may import this package.  It shares no code with the
+CUDA path (``paper_1612_08709_b200``) and never imports it; the only shared
+module is ``synth`` (seeded inputs, no method arithmetic).
+
+Every function follows the paper's pseudocode step by step, in the paper's
+order and notation.  Library primitives used as single steps: matrix products
+(numpy/BLAS), ``numpy.linalg.eigh`` for "Calculate the eigendecomposition"
+(LAPACK dsyevd) and ``numpy.linalg.svd`` for "Calculate the singular value
+decomposition" (LAPACK dgesdd).  The paper treats both as black boxes
+(SPEC.md "Dense kernels: contract-only").
+
+Citations: ``P:n`` = /root/reference/PAPER.md line n.
+
+Readings of the paper taken here (all listed in DESIGN.md "Readings"):
+  R1 working precision wp is an explicit argument, default 1e-11.
+  R2 "Form the Gram matrix" of a row-partitioned matrix = per-partition Gram,
+     summed in a fixed pairwise tree over partitions, then
+     symmetrised (B + B^T)/2.
+  R3 eigenvalues clamped at 0 and sorted descending.
+  R4 Alg. 3's output is sorted by descending Sigma.
+  R5 signs: each (u_j, v_j) flipped so the largest-|.| entry of v_j is positive.
+  R6 Alg. 6's SVD of B = Q^T A (l x n) is Alg. 4 applied to B^T (n x l).
+  R7 Alg. 8 returns the leading k <= l triplets.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+DEFAULT_WP = 1e-11  # P:137-139 "the working precision could be 10^-11"
+
+
+# ---------------------------------------------------------------- helpers --
+def split_rows(m: int, parts: int) -> list[tuple[int, int]]:
+    """Contiguous row partitions (the 'IndexedRowMatrix' partitions)."""
+    parts = max(1, min(parts, max(m, 1)))
+    edges = [(m * p) // parts for p in range(parts + 1)]
+    return [(edges[p], edges[p + 1]) for p in range(parts)]
+
+
+def tree_sum(items: list[np.ndarray]) -> np.ndarray:
+    """Fixed pairwise (left-balanced) tree reduction: 'merging intermediate results
+    through multiple levels of a dependency tree'."""
+    if not items:
+        raise ValueError("tree_sum of an empty list")
+    while len(items) > 1:
+        nxt = [items[i] + items[i + 1] for i in range(0, len(items) - 1, 2)]
+        if len(items) % 2:
+            nxt.append(items[-1])
+        items = nxt
+    return items[0]
+
+
+def gram(a: np.ndarray, parts: int = 1) -> np.ndarray:
+    """Alg. 3/4 step 1: 'Form the Gram matrix B = A^* A'.
+
+    Per-partition A_p^T A_p, aggregated by tree_sum (reading R2), symmetrised.
+    """
+    b = tree_sum([a[s:e].T @ a[s:e] for s, e in split_rows(a.shape[0], parts)])
+    return 0.5 * (b + b.T)
+
+
+def column_norms(a: np.ndarray, parts: int = 1) -> np.ndarray:
+    """Euclidean norms of the columns (Remark 'normalizing'),
+    per-partition sums of squares aggregated by tree_sum."""
+    ss = tree_sum([np.sum(a[s:e] * a[s:e], axis=0) for s, e in split_rows(a.shape[0], parts)])
+    return np.sqrt(ss)
+
+
+def sym_eig(b: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """'Calculate the eigendecomposition B = V D V^*'.
+
+    LAPACK via numpy.linalg.eigh; descending order; D clamped to >= 0 (R3).
+    """
+    if not np.all(np.isfinite(b)):
+        raise ValueError("non-finite input to sym_eig")
+    d, v = np.linalg.eigh(b)
+    order = np.argsort(-d, kind="stable")
+    return np.maximum(d[order], 0.0), v[:, order]
+
+
+def keep_mask(s: np.ndarray, wp: float) -> np.ndarray:
+    """Discard rule of Alg. 3 step 5 / Alg. 4 steps 5 and 11:
+    'view any entry of Sigma as numerically zero that is less than the greatest entry of
+    Sigma times the square root of the working precision'."""
+    if s.size == 0 or s.max() <= 0.0:
+        return np.zeros(s.shape, dtype=bool)
+    return s >= s.max() * np.sqrt(wp)
+
+
+def canonical_signs(u: np.ndarray, v: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """Reading R5: flip (u_j, v_j) so that the largest-magnitude entry of v_j is positive
+    (ties -> lowest index).  The paper is silent on signs."""
+    u = u.copy()
+    v = v.copy()
+    for j in range(v.shape[1]):
+        i = int(np.argmax(np.abs(v[:, j])))
+        if v[i, j] < 0:
+            v[:, j] = -v[:, j]
+            u[:, j] = -u[:, j]
+    return u, v
+
+
+def _check(a: np.ndarray, wp: float) -> None:
+    if a.ndim != 2:
+        raise ValueError("A must be 2-D")
+    if not (0.0 < wp < 1.0):
+        raise ValueError("working precision must lie in (0, 1)")
+    if a.shape[0] < a.shape[1]:
+        raise ValueError("tall-skinny SVD needs m >= n (P:98-104)")
+    if not np.all(np.isfinite(a)):
+        raise ValueError("non-finite entry in A")
+
+
+# ------------------------------------------------------------ Algorithm 3 --
+def alg3(a: np.ndarray, wp: float = DEFAULT_WP, parts: int = 1):
+    """Algorithm 3: Gram-based SVD of a tall and skinny matrix.
+
+    Returns U (m x r), sigma (r, descending), V (n x r).
+    """
+    _check(a, wp)
+    m, n = a.shape
+    # Step 1: Form the Gram matrix B = A^* A.
+    b = gram(a, parts)
+    # Step 2: eigendecomposition B = V D V^*.
+    _, v = sym_eig(b)
+    # Step 3: Form U~ = A V.
+    ut = a @ v
+    # Step 4: Sigma = Euclidean norms of the columns of U~ (Remark 'normalizing').
+    sig = column_norms(ut, parts)
+    # Step 5: discard entries of Sigma below max(Sigma) * sqrt(wp), with the
+    # corresponding columns of U~ and V.
+    keep = keep_mask(sig, wp)
+    sig, ut, v = sig[keep], ut[:, keep], v[:, keep]
+    # Step 6: Form U = U~ Sigma^{-1}.
+    u = ut / sig[None, :] if sig.size else ut
+    # Reading R4: descending Sigma.
+    order = np.argsort(-sig, kind="stable")
+    return u[:, order], sig[order], v[:, order]
+
+
+# ------------------------------------------------------------ Algorithm 4 --
+def alg4(a: np.ndarray, wp: float = DEFAULT_WP, parts: int = 1, return_pass1: bool = False):
+    """Algorithm 4: Gram-based SVD with double orthonormalization.
+
+    Returns U (m x r'), sigma (r', descending), V (n x r') [, Y after pass 1].
+    """
+    _check(a, wp)
+    m, n = a.shape
+    # Step 1: B = A^* A.
+    b = gram(a, parts)
+    # Step 2: B = V~ D~ V~^*.
+    _, vt = sym_eig(b)
+    # Step 3: Y~ = A V~.
+    yt = a @ vt
+    # Step 4: Sigma~ = column norms of Y~.
+    st = column_norms(yt, parts)
+    # Step 5: discard below max(Sigma~) sqrt(wp).
+    keep = keep_mask(st, wp)
+    st, yt, vt = st[keep], yt[:, keep], vt[:, keep]
+    r = st.size
+    if r == 0:
+        z = np.zeros((m, 0)), np.zeros(0), np.zeros((n, 0))
+        return (*z, np.zeros((m, 0))) if return_pass1 else z
+    # Step 6: Y = Y~ Sigma~^{-1}.
+    y = yt / st[None, :]
+    # Step 7: Z = Y^* Y.
+    z = gram(y, parts)
+    # Step 8: Z = W D W^*.
+    _, w = sym_eig(z)
+    # Step 9: Q~ = Y W.
+    qt = y @ w
+    # Step 10: T = column norms of Q~.
+    t = column_norms(qt, parts)
+    # Step 11: discard below max(T) sqrt(wp), with columns of Q~ and W.
+    keep2 = keep_mask(t, wp)
+    t, qt, w = t[keep2], qt[:, keep2], w[:, keep2]
+    # Step 12: Q = Q~ T^{-1}.
+    q = qt / t[None, :]
+    # Step 13: R = T W^* Sigma~ V~^*   (r' x n).
+    rmat = (t[:, None] * w.T) @ (st[:, None] * vt.T)
+    # Step 14: SVD R = P Sigma V^*.
+    p, sig, vh = np.linalg.svd(rmat, full_matrices=False)
+    # Step 15: U = Q P.
+    u = q @ p
+    out = (u, sig, vh.T)
+    return (*out, y) if return_pass1 else out
+
+
+def tssvd(a: np.ndarray, wp: float = DEFAULT_WP, passes: int = 2, parts: int = 1):
+    """Problem {1}: Alg. 4 (passes=2) or Alg. 3 (passes=1), canonical signs (R5)."""
+    if passes not in (1, 2):
+        raise ValueError("passes must be 1 or 2")
+    u, s, v = (alg4 if passes == 2 else alg3)(a, wp, parts)
+    u, v = canonical_signs(u, v)
+    return u, s, v
+
+
+# ------------------------------------------------------- Algorithms 5,6,8 --
+def subspace_iteration(a: np.ndarray, omega: np.ndarray, i: int, wp: float = DEFAULT_WP,
+                       parts: int = 1) -> np.ndarray:
+    """Algorithm 5 with Alg. 3 inside and Alg. 4 in the last step (Alg. 8).
+
+    'we use Q = U and R = Sigma V^*': the orthonormal factor of each
+    tall-skinny factorization is the U returned by Alg. 3 / Alg. 4.
+    """
+    m, n = a.shape
+    l = omega.shape[1]
+    if not (0 < l < min(m, n)) or i < 0:
+        raise ValueError("need 0 < l < min(m, n) and i >= 0 (P:705-707)")
+    # Step 1: Q~_0 = n x l Gaussian (supplied by the caller, shared by both paths).
+    qt = omega
+    for _ in range(i):
+        # Step 3: Y_j = A Q~_{j-1}.
+        y = a @ qt
+        # Step 4: Y_j = Q_j R_j via Alg. 3.
+        q, _, _ = alg3(y, wp, parts)
+        # Step 5: Y~_j = A^* Q_j  (rows aggregated over partitions, tree order).
+        yt = tree_sum([a[s:e].T @ q[s:e] for s, e in split_rows(m, parts)])
+        # Step 6: Y~_j = Q~_j R~_j via Alg. 3.
+        qt, _, _ = alg3(yt, wp, 1)
+    # Step 8: Y = A Q~_i.
+    y = a @ qt
+    # Step 9: Y = Q R with double orthonormalization (Alg. 4).
+    q, _, _ = alg4(y, wp, parts)
+    return q
+
+
+def direct_svd(a: np.ndarray, q: np.ndarray, wp: float = DEFAULT_WP, parts: int = 1):
+    """Algorithm 6.  Reading R6: the SVD of B is Alg. 4 on B^T = A^* Q."""
+    m, n = a.shape
+    # Step 1: B = Q^* A, formed as B^T = A^* Q (rows aggregated over partitions).
+    bt = tree_sum([a[s:e].T @ q[s:e] for s, e in split_rows(m, parts)])
+    # Step 2: B = U~ Sigma V^*  <=>  B^T = V Sigma U~^*.
+    v, sig, ut = alg4(bt, wp, 1)
+    # Step 3: U = Q U~.
+    u = q @ ut
+    return u, sig, v
+
+
+def lowrank_svd(a: np.ndarray, omega: np.ndarray, i: int, k: int | None = None,
+                wp: float = DEFAULT_WP, parts: int = 1):
+    """Algorithm 8 = Alg. 6 fed with Alg. 5 using Alg. 3 and Alg. 4.
+
+    Returns the leading k triplets (reading R7), canonical signs (R5).
+    """
+    l = omega.shape[1]
+    k = l if k is None else k
+    if not (0 < k <= l):
+        raise ValueError("need 0 < k <= l")
+    q = subspace_iteration(a, omega, i, wp, parts)
+    u, s, v = direct_svd(a, q, wp, parts)
+    kk = min(k, s.size)
+    u, v = canonical_signs(u[:, :kk], v[:, :kk])
+    return u, s[:kk], v
