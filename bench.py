@@ -1,0 +1,316 @@
+"""Benchmark of the Gram-based SVD hot path on B200 (driver contract: one JSON line).
+
+  python bench.py [--gpus N --steps K --warmup W] [--config c2] [--impl ours|reference]
+
+A "step" is one whole tall-skinny SVD (Algorithm 4, two Gram passes) of the
+BASELINE.json configs[1] matrix (2,000,000 x 100 FP64, Haar U/V, sigma from 1
+to 1e-10), row-sharded over N GPUs (strong scaling: the matrix is fixed).
+`value` = A-stream throughput: algorithmic bytes of A streamed by the step's
+passes over A (2 for Alg. 4: the Gram pass and the A V~ pass; 2i+2 for Alg. 8)
+divided by the step time, summed over GPUs (whole job).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+MEASURED_FP64_DMMA_TFLOPS = 37.2  # tools/fp64_peak.cu on this pool's B200 (profiles/r01_fp64_peak.txt)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="c2")
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--wp", type=float, default=1e-11)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample-rows", type=int, default=0)
+    return p.parse_args()
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"bench_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        rows = []
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 7:
+                try:
+                    rows.append((float(f[0]), float(f[1]), f[3:7]))
+                except ValueError:
+                    pass
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v == "Active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def a_passes(cfg):
+    return 2 if cfg["kind"] == "tssvd" else 2 * cfg["iters"] + 2
+
+
+# ------------------------------------------------------------ reference --
+def run_reference(args, rank, world):
+    """--impl reference: the oracle (oracle/) as it stands, on the host cores, bounded samples."""
+    if rank != 0:
+        return
+    import oracle
+
+    cfg = synth.CONFIGS[args.config]
+    rows = args.cpu_sample_rows or (200_000 if cfg["kind"] == "tssvd" else 20_000)
+    d = synth.config_inputs(args.config, m=min(rows, cfg["m"]),
+                            n=None if cfg["kind"] == "tssvd" else min(cfg["n"], 4_000))
+    a = d["A"]
+
+    def step():
+        if cfg["kind"] == "tssvd":
+            oracle.tssvd(a, args.wp, 2)
+        else:
+            oracle.lowrank_svd(a, d["Omega"], d["iters"], d["k"], args.wp)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    gbs = a_passes(cfg) * a.nbytes / dt / 1e9
+    sample = f"first {a.shape[0]} rows x {a.shape[1]} cols of {args.config} ({a.nbytes / 1e9:.2f} GB)"
+    line = {"impl": "reference", "metric": metric_name(cfg), "value": round(gbs, 3), "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_obj(args, cfg, world),
+            "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": os.cpu_count(),
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def metric_name(cfg):
+    return "A-stream GB/s (Alg. 4 tall-skinny SVD)" if cfg["kind"] == "tssvd" else \
+        "A-stream GB/s (Alg. 8 low-rank SVD)"
+
+
+def config_obj(args, cfg, world):
+    c = {"workload": f"{args.config}: {cfg['m']}x{cfg['n']} FP64 "
+                     + ("tall-skinny SVD, Alg. 4 (two Gram passes)" if cfg["kind"] == "tssvd"
+                        else f"low-rank SVD Alg. 8, k={cfg['k']} l={cfg['l']} i={cfg['iters']}"),
+         "m": cfg["m"], "n": cfg["n"], "rows_per_gpu": -(-cfg["m"] // world),
+         "working_precision": args.wp, "parallelism": f"row-shard x{world}",
+         "l2": "A is larger than L2 (126 MB) on every rank; no flush needed"}
+    return c
+
+
+# ------------------------------------------------------------ ours -------
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1612_08709_b200 as tk
+    from paper_1612_08709_b200 import _lib
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    comm = tk.Comm(device=local_rank) if world > 1 else None
+    cfg = synth.CONFIGS[args.config]
+    r0, r1 = tk.shard_rows(cfg["m"], world, rank)
+    d = synth.config_inputs(args.config, rows=(r0, r1))
+    a_host = torch.from_numpy(d["A"]).pin_memory()
+    A = a_host.to(dev)
+    m_local, n = A.shape
+    lowrank = cfg["kind"] == "lowrank"
+    if lowrank:
+        om_host = torch.from_numpy(d["Omega"]).pin_memory()
+        Om = om_host.to(dev)
+    U = torch.empty_like(A) if not lowrank else None
+
+    def step():
+        if lowrank:
+            return tk.lowrank_svd(A, Om, cfg["iters"], cfg["k"], wp=args.wp, comm=comm)
+        return tk.tssvd(A, wp=args.wp, passes=2, comm=comm, U=U)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    st = _lib.last_stats()
+    launches = st["kernel_launches"]
+    barrier()
+    clocks = Clocks(local_rank)
+    clocks.start()
+    _lib.set_pass_timing(True)
+    pass_ms = {}
+    pass_flops = {}
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        out = step()
+        for p in _lib.last_stats()["passes"]:
+            pass_ms.setdefault(p["kind"], []).append(p["ms"])
+            pass_flops.setdefault(p["kind"], []).append(p["flops"])
+    e1.record(stream)
+    barrier()
+    _lib.set_pass_timing(False)
+    ck = clocks.stop()
+    t = e0.elapsed_time(e1) / args.steps  # ms per step on this rank
+    tt = torch.tensor([t], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t = tt.item()
+    total_a_bytes = 8.0 * cfg["m"] * cfg["n"] * a_passes(cfg)
+    value = total_a_bytes / (t * 1e-3) / 1e9
+
+    # e2e through the same C-ABI call with HOST buffers (H2D of A, D2H of U/sigma/V inside)
+    e2e = None
+    if not args.no_e2e and not lowrank:
+        ts = []
+        for i in range(args.warmup + args.steps):
+            barrier()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            u_h, s_h, v_h = tk.tssvd(a_host, wp=args.wp, passes=2, comm=comm)
+            s1.record(stream)
+            s1.synchronize()
+            if i >= args.warmup:
+                ts.append(s0.elapsed_time(s1))
+        te = torch.tensor([statistics.mean(ts)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        r = u_h.shape[1]
+        e2e = {"value": round(total_a_bytes / (te.item() * 1e-3) / 1e9, 3), "unit": "GB/s",
+               "ms_per_step": round(te.item(), 3),
+               "h2d_bytes_per_step": int(8 * m_local * n),
+               "d2h_bytes_per_step": int(8 * (m_local * r + r + n * r))}
+
+    # roofline of the dominant kernel (largest share of the step's device time)
+    shares = {k: sum(v) / args.steps for k, v in pass_ms.items()}
+    dom = max((k for k in shares if k != "jacobi"), key=lambda k: shares[k])
+    avg_ms = statistics.mean(pass_ms[dom])
+    flops = statistics.mean(pass_flops[dom])
+    achieved = flops / (avg_ms * 1e-3) / 1e12
+    roof = {"kernel": dom, "bound": "tensor", "achieved": round(achieved, 3),
+            "peak": MEASURED_FP64_DMMA_TFLOPS, "unit": "TFLOP/s",
+            "frac": round(achieved / MEASURED_FP64_DMMA_TFLOPS, 4), "traffic": None,
+            "peak_source": "FP64 DMMA.8x8x4 throughput measured on this pool's B200 by "
+                           "tools/fp64_peak.cu (MEASURED_PEAKS.json has no FP64 entry)",
+            "share_of_step": round(shares[dom] / t, 4),
+            "pass_ms_per_step": {k: round(v, 4) for k, v in sorted(shares.items())}}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args, cfg)
+
+    if rank == 0:
+        line = {"metric": metric_name(cfg), "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t, 4),
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": config_obj(args, cfg, world),
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": ck,
+                "gpu_launches": int(launches * args.steps),
+                "kept_rank": int(out[1].numel()),
+                "jacobi_sweeps": st["jacobi_sweeps"]}
+        print(json.dumps(line), flush=True)
+    if comm:
+        comm.close()
+
+
+def cpu_baseline(args, cfg):
+    """The oracle as it stands, on this host's cores, on a bounded sample (~10-30 s)."""
+    import oracle
+
+    rows = args.cpu_sample_rows or (500_000 if cfg["kind"] == "tssvd" else 20_000)
+    d = synth.config_inputs(args.config, m=min(rows, cfg["m"]),
+                            n=None if cfg["kind"] == "tssvd" else min(cfg["n"], 4_000))
+    a = d["A"]
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        if cfg["kind"] == "tssvd":
+            oracle.tssvd(a, args.wp, 2)
+        else:
+            oracle.lowrank_svd(a, d["Omega"], d["iters"], d["k"], args.wp)
+        reps += 1
+        if time.perf_counter() - t0 > 10.0 or reps >= 20:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": round(a_passes(cfg) * a.nbytes / dt / 1e9, 3), "unit": "GB/s",
+            "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"{reps} oracle runs on the first {a.shape[0]} rows x {a.shape[1]} cols of "
+                      f"{args.config} ({a.nbytes / 1e9:.2f} GB), {dt:.2f} s each"}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank) if args.impl == "ours" else None
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,189 @@
+/*
+ * tssvd.h -- C ABI of the B200 (sm_100a) implementation of the Gram-based
+ * distributed SVD hot path of Li, Kluger & Tygert, arXiv 1612.08709
+ * ("Algorithms for distributed computation of PCA and SVD").
+ *
+ * Citations: P:n = line n of the paper's LaTeX source.
+ *
+ * Conventions (all entry points)
+ *   - Every matrix is FP64, ROW-MAJOR, with an explicit leading dimension
+ *     (elements between consecutive rows).  A tall matrix is ROW-SHARDED:
+ *     rank p of the communicator passes its contiguous block of rows A_p
+ *     (m_local x n); the global matrix is the concatenation over ranks in rank
+ *     order ("IndexedRowMatrix" partitions).
+ *   - Pointers are CUDA DEVICE pointers on the communicator's device unless
+ *     opts->host_io == 1, in which case A/Omega and U/sigma/V are HOST pointers
+ *     (pinned memory recommended) and the library stages them through the
+ *     workspace with cudaMemcpyAsync on `stream`.
+ *   - `stream` is a cudaStream_t (passed as void* to keep this header free of
+ *     CUDA types).  All work is enqueued on it; the call synchronises the
+ *     stream at the rank decisions ("Discard ..." steps) because the kept rank
+ *     is returned on the host, and returns with the outputs complete.
+ *   - The caller owns every buffer (workspace included); nothing is allocated
+ *     inside tssvd() / lowrank_svd().  A and Omega are never written.
+ *   - Errors: every entry point returns a tssvd_status; on failure
+ *     tssvd_last_error() returns a thread-local detail string.  In a
+ *     multi-rank job every rank returns the same status for argument errors
+ *     that depend on global sizes.  Nothing throws across the ABI.
+ */
+#ifndef TSSVD_H_
+#define TSSVD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSSVD_ABI_VERSION 1
+
+typedef enum {
+  TSSVD_OK = 0,
+  TSSVD_EINVAL = 1,     /* bad argument: sizes, leading dimensions, alignment, wp, l, k, iters */
+  TSSVD_ENONFINITE = 2, /* NaN/Inf in A (or Omega), detected on the Gram diagonal */
+  TSSVD_ENOCONV = 3,    /* a Jacobi eigen/SVD core exceeded max_jacobi_sweeps */
+  TSSVD_ECUDA = 4,      /* CUDA runtime error (detail in tssvd_last_error) */
+  TSSVD_ENCCL = 5,      /* NCCL error */
+  TSSVD_ENOMEM = 6      /* workspace_bytes smaller than *_workspace_size() */
+} tssvd_status;
+
+const char* tssvd_status_string(int status);
+const char* tssvd_last_error(void);
+int tssvd_abi_version(void);
+
+/* ---- communicator -------------------------------------------------------
+ * Opaque handle: an NCCL communicator plus rank/size/device.  A NULL comm
+ * means a single-GPU job on the current device (no collectives). */
+typedef struct tssvd_comm tssvd_comm;
+
+/* Rank 0 creates the 128-byte unique id (host memory) and distributes it
+ * out of band (e.g. a torch.distributed broadcast). */
+int tssvd_get_unique_id(unsigned char id[128]);
+/* Collective over `nranks` processes: ncclCommInitRank on `device`. */
+int tssvd_comm_create(int nranks, int rank, const unsigned char id[128], int device,
+                      tssvd_comm** out);
+int tssvd_comm_destroy(tssvd_comm* comm);
+int tssvd_comm_rank(const tssvd_comm* comm, int* rank, int* nranks);
+/* Sum-allreduce of `count` doubles in place on `stream` (exposed for tests). */
+int tssvd_allreduce_sum(tssvd_comm* comm, void* stream, double* buf, int64_t count);
+
+/* ---- options ------------------------------------------------------------ */
+typedef struct {
+  int abi_version;           /* must be TSSVD_ABI_VERSION */
+  double working_precision;  /* wp in (0,1), default 1e-11 ("could be 10^-11") */
+  int orthonormalizations;   /* tssvd: 1 = Algorithm 3, 2 = Algorithm 4 */
+  int max_jacobi_sweeps;     /* cap per small core, e.g. 60; exceeded -> TSSVD_ENOCONV */
+  int host_io;               /* 0: device pointers; 1: host pointers (see conventions) */
+} tssvd_opts;
+
+/* Fills defaults: wp 1e-11, Algorithm 4, 60 sweeps, device pointers. */
+void tssvd_opts_default(tssvd_opts* opts);
+
+/* ---- problem {1}: thin SVD of a tall-skinny matrix ------------
+ * A = U diag(sigma) V^T with U (m x r) and V (n x r) orthonormal columns,
+ * sigma descending, r = kept rank after the "Discard" steps
+ * (Alg. 3 step 5 / Alg. 4 steps 5 and 11: entries below max * sqrt(wp)).
+ * Signs: each (u_j, v_j) is flipped so the largest-|.| entry of v_j is positive.
+ *
+ *   m_local  rows of this rank's shard (>= 0); m = sum over ranks must be >= n
+ *   n        columns, 1 <= n <= 256, n EVEN (rows move as 16-byte TMA granules)
+ *   A        m_local x n, lda >= n, lda even, 16-byte aligned; read-only
+ *   U        m_local x n capacity, ldu >= n, ldu even, 16-byte aligned: columns
+ *            [0, r) receive U_p (sharded like A); the rest is scratch.
+ *            U may alias A (same pointer and ldu == lda): then A is overwritten.
+ *   sigma    n capacity, [0, r) written, replicated on every rank
+ *   V        n x n capacity, ldv >= n: columns [0, r) written, replicated
+ *   rank     HOST out: r (identical on every rank)
+ *   workspace/workspace_bytes: device scratch of at least tssvd_workspace_size()
+ */
+int tssvd_workspace_size(const tssvd_comm* comm, int64_t m_local, int64_t n,
+                         const tssvd_opts* opts, size_t* bytes);
+int tssvd(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, const double* A,
+          int64_t lda, const tssvd_opts* opts, double* U, int64_t ldu, double* sigma, double* V,
+          int64_t ldv, int64_t* rank, void* workspace, size_t workspace_bytes);
+
+/* ---- problem {2}: rank-l approximation, Algorithm 8 ----------
+ * Algorithm 5 (subspace iteration) with Algorithm 3 in its steps 4
+ * and 6 and Algorithm 4 in its last step, fed into Algorithm 6 (P:744-766,
+ * whose SVD of B = Q^T A is Algorithm 4 applied to B^T).  Returns the leading
+ * k <= l triplets with ||A - U diag(sigma) V^T||_2 ~ sigma_{k+1}.
+ *
+ *   n        columns of A, even, n > l
+ *   Omega    n x l start block Q~_0, ldo >= l; must be bit-identical
+ *            on every rank (the caller seeds it)
+ *   l, iters 0 < l < min(m, n), l <= 128; iters >= 0 (the paper's i)
+ *   k        0 < k <= l
+ *   U        m_local x k capacity (ldu >= k), sharded like A
+ *   sigma    k capacity;  V  n x k capacity (ldv >= k), replicated
+ *   rank     HOST out: min(k, kept rank)
+ */
+int lowrank_workspace_size(const tssvd_comm* comm, int64_t m_local, int64_t n, int64_t l,
+                           const tssvd_opts* opts, size_t* bytes);
+int lowrank_svd(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, const double* A,
+                int64_t lda, const double* Omega, int64_t ldo, int64_t l, int iters, int64_t k,
+                const tssvd_opts* opts, double* U, int64_t ldu, double* sigma, double* V,
+                int64_t ldv, int64_t* rank, void* workspace, size_t workspace_bytes);
+
+/* ---- instrumentation ------------------------------------------------------
+ * Per-call counters of the last tssvd()/lowrank_svd() on this thread:
+ * kernel launches enqueued, Jacobi sweeps of each core, and the kept ranks. */
+#define TSSVD_MAX_PASSES 48
+typedef enum {
+  TSSVD_PASS_GRAM_X = 1, /* B = X^T X            (Alg. 3/4 step 1)            */
+  TSSVD_PASS_XV = 2,     /* Y~ = X V~ + norms    (Alg. 3/4 steps 3-4)         */
+  TSSVD_PASS_GRAM_Y = 3, /* Z = Y^T Y            (Alg. 4 step 7)              */
+  TSSVD_PASS_QNORM = 4,  /* norms of Q~ = Y W    (Alg. 4 steps 9-10)          */
+  TSSVD_PASS_UOUT = 5,   /* U = Y~ M (in place)  (Alg. 3 step 6/Alg. 4 st 15) */
+  TSSVD_PASS_ALPHA = 6,  /* Y = A Q~             (Alg. 5 steps 3, 8)          */
+  TSSVD_PASS_BETA = 7,   /* A^T Q                (Alg. 5 step 5, Alg. 6 st 1) */
+  TSSVD_PASS_JACOBI = 8  /* one-sided Jacobi core (eig / SVD)                 */
+} tssvd_pass_kind;
+typedef struct {
+  int64_t kernel_launches;
+  int64_t a_passes;          /* streaming passes over A */
+  int jacobi_sweeps[16];
+  int n_jacobi;
+  int64_t ranks[8];
+  int n_ranks;
+  /* filled only while tssvd_set_pass_timing(1): CUDA-event time of each
+   * streaming pass / Jacobi core, its kind and its ALGORITHMIC flops and bytes */
+  int n_pass;
+  int pass_kind[TSSVD_MAX_PASSES];
+  double pass_ms[TSSVD_MAX_PASSES];
+  double pass_flops[TSSVD_MAX_PASSES];
+  double pass_bytes[TSSVD_MAX_PASSES];
+} tssvd_stats;
+int tssvd_last_stats(tssvd_stats* out);
+/* Enable (1) / disable (0) per-pass CUDA-event timing on this thread. */
+int tssvd_set_pass_timing(int enable);
+
+/* Low-level building blocks, exported for kernel-level parity tests and
+ * benchmarks (device pointers, row-major, `stream` as above). */
+/* G = X^T X (n x n, ldg) over the local rows only (Alg. 3 step 1 before aggregation). */
+int tssvd_gram(void* stream, int64_t m, int64_t n, const double* X, int64_t ldx, double* G,
+               int64_t ldg, void* workspace, size_t workspace_bytes);
+size_t tssvd_gram_workspace(int64_t m, int64_t n);
+/* Y = X M (m x c, ldy), M is k x c (ldm); optional column sums of squares nsq (c). */
+int tssvd_matmul(void* stream, int64_t m, int64_t k, int64_t c, const double* X, int64_t ldx,
+                 const double* M, int64_t ldm, double* Y, int64_t ldy, double* nsq,
+                 void* workspace, size_t workspace_bytes);
+size_t tssvd_matmul_workspace(int64_t m, int64_t k, int64_t c);
+/* Z = X^T Y (n x l, ldz) over the local rows (Alg. 5 step 5 before aggregation). */
+int tssvd_matmul_tn(void* stream, int64_t m, int64_t n, int64_t l, const double* X, int64_t ldx,
+                    const double* Y, int64_t ldy, double* Z, int64_t ldz, void* workspace,
+                    size_t workspace_bytes);
+size_t tssvd_matmul_tn_workspace(int64_t m, int64_t n, int64_t l);
+/* Eigendecomposition of a symmetric POSITIVE SEMIDEFINITE B (n x n, ldb; a
+ * Gram matrix) by one-sided Jacobi on its columns: lambda[j] (descending) and
+ * the unit eigenvectors as ROWS of Vt (n x n, ldv): Vt[j, :] = v_j.
+ * (For an indefinite B, lambda holds |eigenvalues|.) */
+int tssvd_sym_eig(void* stream, int64_t n, const double* B, int64_t ldb, double* lambda,
+                  double* Vt, int64_t ldv, int max_sweeps, int* sweeps, void* workspace,
+                  size_t workspace_bytes);
+size_t tssvd_sym_eig_workspace(int64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSSVD_H_ */

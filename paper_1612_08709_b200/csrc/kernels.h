@@ -1,0 +1,63 @@
+// Internal launcher declarations (not part of the C ABI; see include/tssvd.h).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tsk {
+
+struct DevInfo {
+  int sms = 148;
+  size_t smem_optin = 227 * 1024;
+};
+const DevInfo& dev_info();
+
+// ---- streaming passes over tall row-major matrices (stream_kernels.cu) ----
+// Partial Gram (lower triangle) of X[:, :w] over `grid` contiguous row ranges:
+// part[p][i*wp + j] (i >= j), wp = pad8(w).  Returns the number of partials.
+int syrk_partials_grid(int64_t m, int w);
+size_t syrk_partials_doubles(int64_t m, int w);
+cudaError_t launch_syrk(const double* X, int64_t ldx, int64_t m, int w, double* part,
+                        cudaStream_t s);
+// B = sum_p part[p]  (lower), written symmetric into B (ldb).
+cudaError_t launch_reduce_sym(const double* part, int nparts, int w, double* B, int ldb,
+                              cudaStream_t s);
+
+// Y[:, :c] = X[:, :k] * M  (M row-major, ld = smem_ld(c), rows padded to mult. of 32
+// with zeros).  Optional column sums of squares partials norm_part[g][pad8(c)].
+// In place (Y == X, ldy == ldx) is allowed.
+int gemm_nn_grid(int64_t m, int c);
+cudaError_t launch_gemm_nn(const double* X, int64_t ldx, int64_t m, int k, const double* M,
+                           int c, double* Y, int64_t ldy, double* norm_part, cudaStream_t s);
+size_t gemm_nn_m_doubles(int k, int c);  // size of the padded M buffer
+
+// Z (n x l, ld ldz) partials: Zp[split][n_pad x ldz] = X[rows, :n]^T * Y[rows, :l]
+// reduced over `splits` row ranges.
+struct TnPlan {
+  int cb, mi, nbl, colblocks, splits, kr, nst, ldz;
+  int64_t rows_per_split;
+  size_t part_doubles;
+};
+TnPlan plan_gemm_tn(int64_t m, int n, int l);
+cudaError_t launch_gemm_tn(const TnPlan& p, const double* X, int64_t ldx, int64_t m, int n,
+                           const double* Y, int64_t ldy, int l, double* part, cudaStream_t s);
+// out[e] = sum_p part[p*stride + e] for e < len (fixed two-level order)
+cudaError_t launch_reduce_parts(const double* part, int nparts, int64_t stride, int64_t len,
+                                double* out, cudaStream_t s);
+
+// ---- one-sided Jacobi (jacobi.cu) ----
+// EIG: B (n x n, ldb, symmetric PSD) -> k <= n eigenpairs: vals[j] descending,
+// eigenvector j (unit) contiguous at vecs + j*ldv.  Pivoted-Cholesky
+// preconditioned; pivots <= trunc * max(diag B) are dropped (k = info[2]).
+// info = {sweeps, converged, k}.  vecs may alias B.
+cudaError_t launch_jacobi_eig(const double* B, int ldb, int n, double tol, double trunc,
+                              int max_sweeps, double* vecs, int ldv, double* vals, int* info,
+                              cudaStream_t s);
+// SVD of K given by N columns of length ldot (column j contiguous at cols + j*ldc):
+// K J = P diag(vals), vals descending.  Output column r (ld ldout >= ldot + N):
+// [P(:, r) unit (ldot) ; J(:, r) (N)].  info = {sweeps, converged, N}.
+cudaError_t launch_jacobi_svd(const double* cols, int ldc, int N, int ldot, double tol,
+                              int max_sweeps, double* out, int ldout, double* vals, int* info,
+                              cudaStream_t s);
+
+}  // namespace tsk

@@ -1,0 +1,284 @@
+// Small replicated-core kernels of Alg. 3/4 (everything between the streaming
+// passes that is not the Jacobi solver itself): symmetrisation, the "Discard"
+// decisions, and the assembly of the small n x r factors.  All of them run on
+// data that is bit-identical on every rank, in a fixed order.
+#include <cstdint>
+
+#include "common.cuh"
+#include "small_kernels.h"
+
+namespace tsk {
+
+// B[j][i] = B[i][j] for i > j (NCCL sums the two triangles in different orders).
+__global__ void k_symmetrize(double* B, int w, int ldb) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= w * w) return;
+  const int i = e / w, j = e % w;
+  if (i > j) B[(size_t)j * ldb + i] = B[(size_t)i * ldb + j];
+}
+
+// Row-major padded M (mrows x ldm, zero outside) from column-major cols (c columns of length k, ldc):
+// M[i][j] = cols[j*ldc + i].
+__global__ void k_cols_to_m(const double* cols, int ldc, int k, int c, double* M, int ldm,
+                            int mrows) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)mrows * ldm) return;
+  const int i = (int)(e / ldm), j = (int)(e % ldm);
+  M[e] = (i < k && j < c) ? cols[(size_t)j * ldc + i] : 0.0;
+}
+
+// Row-major padded M from a row-major source (k x c, lds).
+__global__ void k_rows_to_m(const double* src, int64_t lds, int k, int c, double* M, int ldm,
+                            int mrows) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)mrows * ldm) return;
+  const int i = (int)(e / ldm), j = (int)(e % ldm);
+  M[e] = (i < k && j < c) ? src[(size_t)i * lds + j] : 0.0;
+}
+
+// Discard rule.  One CTA.
+//   sig_j = sqrt(nsq_j); keep j iff sig_j >= max(sig) * sqrt(wp) (and max > 0).
+//   idx = kept indices in ascending order; out[0] = r, out[1] = nc = max kept + 1,
+//   out[2] |= 1 if the Gram diagonal (gdiag, stride gld+1) is non-finite.
+__global__ void k_discard(const double* nsq, int w, double sqrt_wp, double* sig, int* idx,
+                          int* out, const double* gdiag, int gld) {
+  __shared__ double smax[32];
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  double mx = 0.0;
+  for (int j = threadIdx.x; j < w; j += blockDim.x) {
+    const double v = nsq[j];
+    const double s = sqrt(fmax(v, 0.0));
+    sig[j] = s;
+    if (!isfinite(v)) bad = 1;
+    if (gdiag && !isfinite(gdiag[(size_t)j * (gld + 1)])) bad = 1;
+    mx = fmax(mx, s);
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) smax[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int q = 0; q < (int)(blockDim.x + 31) / 32; ++q) m = fmax(m, smax[q]);
+    const double thr = m * sqrt_wp;
+    int r = 0, nc = 0;
+    if (m > 0.0 && !bad) {
+      for (int j = 0; j < w; ++j)
+        if (sig[j] >= thr) {
+          idx[r++] = j;
+          nc = j + 1;
+        }
+    }
+    out[0] = r;
+    out[1] = nc;
+    out[2] = bad;
+  }
+}
+
+// Sign of column a: +1/-1 so that its largest-|.| entry (ties -> lowest index) is positive.
+__device__ double col_sign(const double* x, int stride, int len) {
+  int best = 0;
+  double bv = -1.0;
+  for (int i = 0; i < len; ++i) {
+    const double v = fabs(x[(size_t)i * stride]);
+    if (v > bv) bv = v, best = i;
+  }
+  return x[(size_t)best * stride] < 0.0 ? -1.0 : 1.0;
+}
+
+// Alg. 3 outputs with reading R4 (sort by Sigma descending) and R5 (signs).
+// Vt: eigenvectors, column-major (column j at Vt + j*w).  One thread per kept column.
+//   rank_a = position of kept column a by descending sig (ties by index)
+//   M[idx_a][rank_a] = s_a / sig[idx_a];  V[:, rank_a] = s_a * Vt[:, idx_a];  sigma[rank_a] = sig
+__global__ void k_alg3_out(const double* sig, const int* idx, int r, const double* Vt, int w,
+                           double* M, int ldm, double* sigma, double* V, int64_t ldv) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= r) return;
+  const int ja = idx[a];
+  const double sa = sig[ja];
+  int rk = 0;
+  for (int b = 0; b < r; ++b) {
+    const double sb = sig[idx[b]];
+    rk += (sb > sa) || (sb == sa && b < a);
+  }
+  const double* v = Vt + (size_t)ja * w;
+  const double sg = col_sign(v, 1, w);
+  M[(size_t)ja * ldm + rk] = sg / sa;
+  sigma[rk] = sa;
+  for (int i = 0; i < w; ++i) V[(size_t)i * ldv + rk] = sg * v[i];
+}
+
+// Z[a][b] = G[idx_a][idx_b] / (sig_a sig_b) -- Gram of Y = Y~_keep Sigma~^-1.
+__global__ void k_build_z(const double* G, int ldg, const int* idx, const double* sig, int r,
+                          double* Z) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= r * r) return;
+  const int a = e / r, b = e % r;
+  const int ia = idx[a], ib = idx[b];
+  Z[e] = G[(size_t)ia * ldg + ib] / (sig[ia] * sig[ib]);
+}
+
+// M1 (nc x r, row-major padded): M1[idx_a][b] = W(a, b) / sig[idx_a] so that
+// Y~[:, :nc] M1 = Y~_keep Sigma~^-1 W = Y W = Q~.  W column-major (r x r).
+__global__ void k_build_m1(const double* W, const int* idx, const double* sig, int r, int kz,
+                           double* M1, int ldm) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= r * kz) return;
+  const int a = e / kz, b = e % kz;
+  const int ia = idx[a];
+  M1[(size_t)ia * ldm + b] = W[(size_t)b * r + a] / sig[ia];
+}
+
+// Columns of K = T_keep W_keep^T Sigma~ (r2 x r) for the SVD of R = K V~_keep^T
+// (reading R13): column b (length r2) at Kc + b*r2,
+//   K[a][b] = T[idx2_a] * W(b, idx2_a) * sig[idx_b].   W column-major (r x kz).
+__global__ void k_build_k(const double* T, const int* idx2, int r2, const double* W, int r,
+                          const double* sig, const int* idx, double* Kc) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= r2 * r) return;
+  const int b = e / r2, a = e % r2;
+  const int c2 = idx2[a];
+  Kc[e] = T[c2] * W[(size_t)c2 * r + b] * sig[idx[b]];
+}
+
+// After the Jacobi SVD of K (column a of `cols`: [P(:, a) (r2) ; J(:, a) (r)]):
+//   V(:, a) = V~_keep J(:, a)  (R = P Sigma (V~_keep J)^T), sign fixed (R5),
+//   sigma[a], V (row-major, ldv), Ps = P * signs (column-major r2 x r2).
+// One warp per output column a < r2.
+__global__ void k_svd_out(const double* cols, int ldc, int r2, int r, const double* vals,
+                          const double* Vt, int w, const int* idx, double* sigma, double* V,
+                          int64_t ldv, double* Ps) {
+  const int a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (a >= r2) return;
+  const double* x = cols + (size_t)a * ldc;
+  // V(:, a) = sum_b Vt(:, idx_b) J(b, a); find the sign from the largest |entry|
+  double best = -1.0, bestv = 0.0;
+  int besti = 1 << 30;
+  for (int i = lane; i < w; i += 32) {
+    double v = 0.0;
+    for (int b = 0; b < r; ++b) v = fma(Vt[(size_t)idx[b] * w + i], x[r2 + b], v);
+    const double av = fabs(v);
+    if (av > best || (av == best && i < besti)) best = av, bestv = v, besti = i;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const double ov = __shfl_xor_sync(0xffffffffu, bestv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, besti, o);
+    if (ob > best || (ob == best && oi < besti)) best = ob, bestv = ov, besti = oi;
+  }
+  const double sg = bestv < 0.0 ? -1.0 : 1.0;
+  for (int i = lane; i < w; i += 32) {
+    double v = 0.0;
+    for (int b = 0; b < r; ++b) v = fma(Vt[(size_t)idx[b] * w + i], x[r2 + b], v);
+    V[(size_t)i * ldv + a] = sg * v;
+  }
+  for (int c = lane; c < r2; c += 32) Ps[(size_t)a * r2 + c] = sg * x[c];
+  if (lane == 0) sigma[a] = vals[a];
+}
+
+// M2 (nc x r2 row-major padded): M2[idx_b][a] = sum_c W(b, idx2_c) / (sig[idx_b] T[idx2_c]) Ps(c, a)
+// so that Y~[:, :nc] M2 = Q~_keep T^-1 P = Q P = U.
+__global__ void k_build_m2(const double* W, int r, const int* idx, const double* sig,
+                           const double* T, const int* idx2, int r2, const double* Ps, double* M2,
+                           int ldm) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= r * r2) return;
+  const int b = e / r2, a = e % r2;
+  const int ib = idx[b];
+  double s = 0.0;
+  for (int c = 0; c < r2; ++c) {
+    const int c2 = idx2[c];
+    s = fma(W[(size_t)c2 * r + b] / T[c2], Ps[(size_t)a * r2 + c], s);
+  }
+  M2[(size_t)ib * ldm + a] = s / sig[ib];
+}
+
+// Low-rank final step: flip (V_A[:, a], Ut(:, a)) so V_A's largest entry is positive (R5),
+// V_A row-major (n x ?, ldva), Ut row-major (r3 x r4, ldu_t).  One thread per column.
+__global__ void k_canon_lowrank(double* VA, int64_t ldva, int n, double* Ut, int ldut, int r3,
+                                int r4) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= r4) return;
+  const double sg = col_sign(VA + a, (int)ldva, n);
+  if (sg < 0) {
+    for (int i = 0; i < n; ++i) VA[(size_t)i * ldva + a] = -VA[(size_t)i * ldva + a];
+    for (int i = 0; i < r3; ++i) Ut[(size_t)i * ldut + a] = -Ut[(size_t)i * ldut + a];
+  }
+}
+
+// 2-D strided copy (row-major), rows x cols.
+__global__ void k_copy2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
+                         int cols) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= rows * cols) return;
+  const int64_t i = e / cols;
+  const int j = (int)(e % cols);
+  dst[i * ldd + j] = src[i * lds + j];
+}
+
+__global__ void k_fill(double* p, int64_t n, double v) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) p[e] = v;
+}
+
+// ---------------------------------------------------------------- launchers --
+static inline unsigned nb(int64_t n, int b = 256) { return (unsigned)((n + b - 1) / b); }
+
+void symmetrize(double* B, int w, int ldb, cudaStream_t s) {
+  k_symmetrize<<<nb((int64_t)w * w), 256, 0, s>>>(B, w, ldb);
+}
+void cols_to_m(const double* cols, int ldc, int k, int c, double* M, int ldm, int mrows,
+               cudaStream_t s) {
+  k_cols_to_m<<<nb((int64_t)mrows * ldm), 256, 0, s>>>(cols, ldc, k, c, M, ldm, mrows);
+}
+void rows_to_m(const double* src, int64_t lds, int k, int c, double* M, int ldm, int mrows,
+               cudaStream_t s) {
+  k_rows_to_m<<<nb((int64_t)mrows * ldm), 256, 0, s>>>(src, lds, k, c, M, ldm, mrows);
+}
+void discard(const double* nsq, int w, double wp, double* sig, int* idx, int* out,
+             const double* gdiag, int gld, cudaStream_t s) {
+  k_discard<<<1, 256, 0, s>>>(nsq, w, sqrt(wp), sig, idx, out, gdiag, gld);
+}
+void alg3_out(const double* sig, const int* idx, int r, const double* Vt, int w, double* M, int ldm,
+              double* sigma, double* V, int64_t ldv, cudaStream_t s) {
+  k_alg3_out<<<nb(r, 64), 64, 0, s>>>(sig, idx, r, Vt, w, M, ldm, sigma, V, ldv);
+}
+void build_z(const double* G, int ldg, const int* idx, const double* sig, int r, double* Z,
+             cudaStream_t s) {
+  k_build_z<<<nb((int64_t)r * r), 256, 0, s>>>(G, ldg, idx, sig, r, Z);
+}
+void build_m1(const double* W, const int* idx, const double* sig, int r, int kz, double* M1,
+              int ldm, cudaStream_t s) {
+  k_build_m1<<<nb((int64_t)r * kz), 256, 0, s>>>(W, idx, sig, r, kz, M1, ldm);
+}
+void build_k(const double* T, const int* idx2, int r2, const double* W, int r, const double* sig,
+             const int* idx, double* Kc, cudaStream_t s) {
+  k_build_k<<<nb((int64_t)r2 * r), 256, 0, s>>>(T, idx2, r2, W, r, sig, idx, Kc);
+}
+void svd_out(const double* cols, int ldc, int r2, int r, const double* vals, const double* Vt,
+             int w, const int* idx, double* sigma, double* V, int64_t ldv, double* Ps,
+             cudaStream_t s) {
+  k_svd_out<<<nb((int64_t)r2 * 32, 256), 256, 0, s>>>(cols, ldc, r2, r, vals, Vt, w, idx, sigma, V,
+                                                     ldv, Ps);
+}
+void build_m2(const double* W, int r, const int* idx, const double* sig, const double* T,
+              const int* idx2, int r2, const double* Ps, double* M2, int ldm, cudaStream_t s) {
+  k_build_m2<<<nb((int64_t)r * r2), 256, 0, s>>>(W, r, idx, sig, T, idx2, r2, Ps, M2, ldm);
+}
+void canon_lowrank(double* VA, int64_t ldva, int n, double* Ut, int ldut, int r3, int r4,
+                   cudaStream_t s) {
+  k_canon_lowrank<<<nb(r4, 64), 64, 0, s>>>(VA, ldva, n, Ut, ldut, r3, r4);
+}
+void copy2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int cols,
+            cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return;
+  k_copy2d<<<nb(rows * cols), 256, 0, s>>>(src, lds, dst, ldd, rows, cols);
+}
+void fill(double* p, int64_t n, double v, cudaStream_t s) {
+  if (n <= 0) return;
+  k_fill<<<nb(n), 256, 0, s>>>(p, n, v);
+}
+
+}  // namespace tsk

@@ -1,0 +1,227 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Run with `pytest -m gpu` on a B200."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from parity import assert_tssvd_parity, col_dist
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # collected on CPU boxes, skipped there
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1612_08709_b200 as tk  # noqa: E402
+from paper_1612_08709_b200._lib import TssvdError  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+
+
+def to_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def run_tssvd(a, wp, passes, **kw):
+    u, s, v = tk.tssvd(to_dev(a), wp=wp, passes=passes, **kw)
+    torch.cuda.synchronize()
+    return u.cpu().numpy(), s.cpu().numpy(), v.cpu().numpy()
+
+
+# ------------------------------------------------------------ kernels -----
+@pytest.mark.parametrize("m,n", [(1, 2), (31, 10), (4000, 10), (100_003, 100), (65_537, 200),
+                                 (5000, 26), (3000, 60), (20_000, 256)])
+def test_gram_kernel_vs_oracle(m, n):
+    rng = np.random.default_rng(m + n)
+    a = rng.standard_normal((m, n))
+    g = tk.gram(to_dev(a)).cpu().numpy()
+    ref = oracle.gram(a)
+    assert np.array_equal(g, g.T)
+    assert np.max(np.abs(g - ref)) <= 1e-13 * max(1.0, np.max(np.abs(ref))) * max(1, np.sqrt(m) / 10)
+
+
+@pytest.mark.parametrize("m,k,c", [(1, 2, 1), (777, 10, 9), (100_003, 100, 100), (50_001, 200, 200),
+                                   (10_000, 100, 55), (3_001, 256, 256), (1000, 20_000, 25),
+                                   (999, 4_000, 60)])
+def test_matmul_kernel_vs_numpy(m, k, c):
+    rng = np.random.default_rng(m + k + c)
+    x = rng.standard_normal((m, k + (k & 1)))[:, :k] if k & 1 else rng.standard_normal((m, k))
+    mm = rng.standard_normal((k, c))
+    X = to_dev(rng.standard_normal((m, k)))
+    y, nsq = tk.matmul(X, to_dev(mm), norms=True)
+    xr = X.cpu().numpy()
+    ref = xr @ mm
+    y = y.cpu().numpy()
+    scale = np.abs(xr) @ np.abs(mm)
+    assert np.all(np.abs(y - ref) <= 1e-14 * k * scale + 1e-300)
+    assert np.allclose(nsq.cpu().numpy(), np.sum(ref * ref, axis=0), rtol=1e-12, atol=0)
+
+
+def test_matmul_in_place():
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((10_000, 100))
+    mm = rng.standard_normal((100, 60))
+    X = to_dev(x)
+    y = tk.matmul(X, to_dev(mm), out=X)
+    assert y.data_ptr() == X.data_ptr()
+    assert np.allclose(y.cpu().numpy(), x @ mm, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("m,n,l", [(1, 2, 1), (1000, 512, 25), (20_011, 2_000, 25), (5_000, 4_000, 60),
+                                   (3_000, 1_000, 128), (300, 20_000, 32)])
+def test_matmul_tn_kernel_vs_numpy(m, n, l):
+    rng = np.random.default_rng(m + n + l)
+    x = rng.standard_normal((m, n))
+    y = rng.standard_normal((m, l + (l & 1)))
+    z = tk.matmul_tn(to_dev(x), to_dev(y), l).cpu().numpy()
+    ref = x.T @ y[:, :l]
+    assert np.all(np.abs(z - ref) <= 1e-14 * m * (np.abs(x).T @ np.abs(y[:, :l])) + 1e-300)
+
+
+@pytest.mark.parametrize("n", [2, 9, 10, 55, 100, 128, 200, 256])
+def test_jacobi_eig_properties(n):
+    """B V = V diag(lambda), V^T V = I, and lambda vs LAPACK on a well-conditioned Gram."""
+    rng = np.random.default_rng(n)
+    a = rng.standard_normal((3 * n, n))
+    b = a.T @ a
+    lam, v, sweeps = tk.sym_eig(to_dev(b))
+    lam, v = lam.cpu().numpy(), v.cpu().numpy()
+    assert np.all(np.diff(lam) <= 0)
+    assert np.max(np.abs(v.T @ v - np.eye(n))) <= 1e-13
+    assert np.max(np.abs(b @ v - v * lam)) <= 1e-13 * lam[0]
+    d, _ = oracle.sym_eig(b)
+    assert np.max(np.abs(lam - d)) <= 1e-13 * d[0]
+    assert sweeps < 30
+
+
+# ---------------------------------------------------------- tssvd ---------
+@pytest.mark.parametrize("wp,r", [(1e-11, 9), (1e-14, 10)])
+@pytest.mark.parametrize("passes", [1, 2])
+def test_tssvd_c1(wp, r, passes):
+    d = synth.config_inputs("c1")
+    a = d["A"]
+    gpu = run_tssvd(a, wp, passes)
+    ref = oracle.tssvd(a, wp, passes)
+    assert ref[1].size == r
+    assert_tssvd_parity(gpu, ref, passes=passes)
+    assert np.max(np.abs(gpu[1] - d["sigma"][:r])) <= 1e-12
+
+
+@pytest.mark.parametrize("passes", [1, 2])
+def test_tssvd_c2_reduced(passes):
+    d = synth.config_inputs("c2", m=200_000)
+    gpu = run_tssvd(d["A"], 1e-11, passes)
+    ref = oracle.tssvd(d["A"], 1e-11, passes)
+    assert ref[1].size == 55
+    assert_tssvd_parity(gpu, ref, passes=passes)
+
+
+def test_tssvd_c4_reduced():
+    d = synth.config_inputs("c4", m=300_000)
+    gpu = run_tssvd(d["A"], 1e-11, 2)
+    ref = oracle.tssvd(d["A"], 1e-11, 2)
+    assert ref[1].size == 92
+    assert_tssvd_parity(gpu, ref, passes=2)
+
+
+@pytest.mark.slow
+def test_tssvd_c2_full_size():
+    """BASELINE configs[1] at full size (2e6 x 100), the bench workload, against the oracle."""
+    d = synth.config_inputs("c2")
+    gpu = run_tssvd(d["A"], 1e-11, 2)
+    ref = oracle.tssvd(d["A"], 1e-11, 2)
+    info = assert_tssvd_parity(gpu, ref, passes=2)
+    assert np.max(np.abs(gpu[1] - d["sigma"][:55])) <= 1e-12
+    print(info)
+
+
+@pytest.mark.parametrize("m,n", [(2, 2), (33, 32), (1000, 2), (12_345, 18), (70_001, 64), (4_097, 130),
+                                 (9_999, 256)])
+def test_tssvd_ragged_random(m, n):
+    rng = np.random.default_rng(m * 7 + n)
+    a = rng.standard_normal((m, n)) * np.exp(-np.arange(n) / 4.0)[None, :]
+    gpu = run_tssvd(a, 1e-11, 2)
+    ref = oracle.tssvd(a, 1e-11, 2)
+    assert_tssvd_parity(gpu, ref, passes=2)
+
+
+def test_tssvd_rank_deficient_and_duplicates():
+    rng = np.random.default_rng(11)
+    a = rng.standard_normal((5000, 6)) @ rng.standard_normal((6, 40))
+    a[:, 7] = a[:, 3]
+    gpu = run_tssvd(a, 1e-11, 2)
+    ref = oracle.tssvd(a, 1e-11, 2)
+    assert ref[1].size == 6
+    assert_tssvd_parity(gpu, ref, passes=2)
+
+
+def test_tssvd_zero_matrix_and_errors():
+    u, s, v = tk.tssvd(torch.zeros((100, 10), dtype=torch.float64, device=DEV))
+    assert s.numel() == 0
+    bad = torch.ones((100, 10), dtype=torch.float64, device=DEV)
+    bad[5, 3] = float("nan")
+    with pytest.raises(TssvdError, match="ENONFINITE"):
+        tk.tssvd(bad)
+    with pytest.raises(TssvdError, match="EINVAL"):
+        tk.tssvd(torch.ones((100, 9), dtype=torch.float64, device=DEV))  # odd n
+    with pytest.raises(TssvdError, match="EINVAL"):
+        tk.tssvd(torch.ones((8, 10), dtype=torch.float64, device=DEV))  # wide
+
+
+def test_tssvd_host_io_matches_device():
+    d = synth.config_inputs("c1")
+    a = torch.from_numpy(d["A"])
+    uh, sh, vh = tk.tssvd(a.pin_memory())
+    ud, sd, vd = tk.tssvd(a.to(DEV))
+    assert torch.equal(sh, sd.cpu()) and torch.equal(vh, vd.cpu()) and torch.equal(uh, ud.cpu())
+
+
+def test_tssvd_deterministic():
+    d = synth.config_inputs("c2", m=100_000)
+    r1 = run_tssvd(d["A"], 1e-11, 2)
+    r2 = run_tssvd(d["A"], 1e-11, 2)
+    for x, y in zip(r1, r2):
+        assert np.array_equal(x, y)
+
+
+# ------------------------------------------------------ low rank ----------
+def lowrank_gpu(a, om, iters, k, wp=1e-11):
+    u, s, v = tk.lowrank_svd(to_dev(a), to_dev(om), iters, k, wp=wp)
+    torch.cuda.synchronize()
+    return u.cpu().numpy(), s.cpu().numpy(), v.cpu().numpy()
+
+
+@pytest.mark.parametrize("name,m,n", [("c3", 20_000, 4_000), ("c5", 25_000, 4_000)])
+def test_lowrank_reduced_configs(name, m, n):
+    d = synth.config_inputs(name, m=m, n=n)
+    gpu = lowrank_gpu(d["A"], d["Omega"], d["iters"], d["k"])
+    ref = oracle.lowrank_svd(d["A"], d["Omega"], d["iters"], d["k"])
+    assert gpu[1].size == ref[1].size == d["k"]
+    s1 = ref[1][0]
+    assert np.max(np.abs(gpu[1] - ref[1])) <= 1e-10 * s1
+    assert oracle.ortho_error(gpu[0]) <= 1e-13 and oracle.ortho_error(gpu[2]) <= 1e-13
+    eg = oracle.spectral_error(d["A"], *gpu, d["x0"])
+    er = oracle.spectral_error(d["A"], *ref, d["x0"])
+    assert abs(eg - er) <= 0.01 * er
+    assert np.all(col_dist(gpu[2], ref[2]) <= 1e-6)
+
+
+@pytest.mark.parametrize("iters", [0, 1])
+def test_lowrank_iters_edge(iters):
+    d = synth.config_inputs("c3", m=6_000, n=1_000)
+    gpu = lowrank_gpu(d["A"], d["Omega"], iters, 20)
+    ref = oracle.lowrank_svd(d["A"], d["Omega"], iters, 20)
+    assert gpu[1].size == ref[1].size
+    assert np.max(np.abs(gpu[1] - ref[1])) <= 1e-10 * ref[1][0]
+
+
+def test_lowrank_paper_table8_pin():
+    """PAPER.md:1040 (Table 8, Alg. 8, m=1e4, n=2000, l=20, i=2): 4.83e-07 on the GPU path."""
+    a, sig = synth.paper_lowrank_test_matrix(10_000, 2_000, 20)
+    om = synth.omega(2_000, 20, 100)
+    gpu = lowrank_gpu(a, om, 2, 20)
+    ref = oracle.lowrank_svd(a, om, 2, 20)
+    assert gpu[1].size == ref[1].size == 6
+    err = oracle.spectral_error(a, *gpu, synth.power_start(2_000, 7))
+    assert err == pytest.approx(4.83e-07, rel=5e-3)
