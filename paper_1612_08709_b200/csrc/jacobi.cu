@@ -1,30 +1,38 @@
-// Small replicated cores of Alg. 3/4 on one CTA cluster (sm_100a):
+// Small replicated cores of Alg. 3/4 on one CTA or one CTA cluster (sm_100a):
 //
 //   EIG mode -- "Calculate the eigendecomposition B = V D V^*" (PAPER.md:615-617,
 //     648-650, 670-672) of a symmetric positive semidefinite Gram matrix:
-//       1. diagonally pivoted Cholesky  B = R^T R, stopped when the largest
-//          remaining pivot is <= trunc * max_i B_ii (k <= n rows);
-//       2. one-sided (Hestenes) Jacobi on the k columns of R^T:
-//          R^T J = X with mutually orthogonal columns, so X = V diag(s) and
-//          B = V diag(s^2) V^T on the range kept.  Eigenvectors are the
-//          normalised columns of X (no accumulator), eigenvalues s^2.
-//     The pivoted Cholesky is the preconditioner of one-sided Jacobi
-//     (Drmac-Veselic): R^T is graded, Jacobi converges in ~8 sweeps instead of
-//     ~30 on B itself, and columns below trunc (numerically null directions,
-//     which the paper's discard step would drop anyway) never enter.
+//       1. diagonally pivoted Cholesky  B = X X^T (X = R^T, n x K), stopped when
+//          the largest remaining pivot is <= trunc * max_i B_ii;
+//       2. one-sided (Hestenes) Jacobi on the K columns of X:  X J = Y with
+//          mutually orthogonal columns, so B = Y Y^T = V diag(|y_j|^2) V^T.
+//          Eigenvectors are the normalised columns of Y (no accumulator).
+//     The pivoted Cholesky preconditions one-sided Jacobi (Drmac-Veselic):
+//     X is graded, Jacobi converges in ~8 sweeps instead of ~20-30 on B, and
+//     numerically null directions (which the paper's discard step drops
+//     anyway) never enter.
 //   SVD mode -- "Calculate the singular value decomposition" of a
-//     small matrix given by columns, rotations accumulated into an appended
+//     small matrix K given by columns, rotations accumulated into an appended
 //     identity block: K J = P diag(sigma), so K = P diag(sigma) J^T.
 //
-// Storage: all slots (columns) live in the distributed shared memory of a
-// cluster of C CTAs (slot s in CTA s % C).  A round of the round-robin
-// (circle) ordering rotates N/2 disjoint pairs in parallel, one group of G
-// lanes per pair; rounds end with a barrier (cluster barrier when C > 1).
-// Rotation test: |x_p^T x_q| > tol ||x_p|| ||x_q||.  Every reduction has a
-// fixed order: all ranks compute bit-identical results from identical inputs.
+// Layout.  Every column ("slot") is stored contiguously in shared memory.
+// With a cluster of C CTAs the ROWS are split: CTA h holds rows
+// [h*Lh, (h+1)*Lh) of every slot.  A Jacobi round rotates all pairs of the
+// round-robin (circle) ordering in parallel, one group of G lanes per pair;
+// the three dot products of a pair are reduced over the group by an xor
+// butterfly (bit-identical in every lane) and, for C > 1, summed over the
+// cluster in CTA order through distributed shared memory.  Every reduction has
+// a fixed order, so every rank computes bit-identical results from identical
+// inputs, and all CTAs of a cluster take identical rotation decisions.
+//
+// Cost model (B200: 64 FP64 FMA/clk/SM): a round is ~7 L FMAs per pair, spread
+// over all 16 warps; C = 1 rounds end in one __syncthreads, C > 1 rounds add one
+// DSMEM exchange and one cluster barrier (~600 cycles), so clusters are used
+// only when a single CTA's 227 KB cannot hold the columns.
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -33,299 +41,424 @@ namespace cg = cooperative_groups;
 
 namespace tsk {
 
-static constexpr int JAC_THREADS = 512;
-static constexpr int JAC_WARPS = JAC_THREADS / 32;
-static constexpr int JAC_MAXSLOTS = 256;  // per CTA
+static constexpr int JT = 512;          // threads per CTA
+static constexpr int JW = JT / 32;      // warps per CTA
+static constexpr int JMAX = 256;        // max slots (columns)
+static constexpr int JMAXP = JMAX / 2;  // max pairs per round
 
-struct JacShared {
-  double red_d[JAC_WARPS];
-  int red_i[JAC_WARPS];
-  double cta_val[2];  // per-CTA partial results read by the other CTAs
-  int cta_idx;
-  int flag[3];
-  int piv_flag[JAC_MAXSLOTS];
-  double nrm[512];
-  int rank_out[512];
-  int order[512];  // global column index -> slot (EIG: pivot order)
-  double bcast[512];  // local copy of the current pivot row
-  double mu, thresh, nu2;
-  int k;
+struct JacArgs {
+  const double* in;
+  int ldin;
+  int mode;  // 0 = EIG, 1 = SVD
+  int n;     // EIG: order of B
+  int N;     // SVD: number of columns
+  int ldot;  // SVD: rows of K (dot-product rows); EIG: n
+  int dpad;  // rows entering dot products, rounded up to even (accumulator starts here)
+  int L;     // total rows per slot (EIG: n; SVD: dpad + N)
+  int Lh;    // rows per CTA (even)
+  int P;     // slot pitch in doubles (= 2 G V >= Lh)
+  int V;     // double2 per lane per slot in the sweeps (= template V)
+  double tol, trunc;
+  int max_sweeps;
+  double* out;
+  int ldout;
+  double* vals;
+  int* info;
 };
 
-template <int G, int EPG>
-__global__ void __launch_bounds__(JAC_THREADS) jacobi_kernel(const double* __restrict__ in,
-                                                           int ldin, int mode, int n, int N,
-                                                           int ldot, int lacc, double tol,
-                                                           double trunc, int max_sweeps,
-                                                           double* __restrict__ out, int ldout,
-                                                           double* __restrict__ vals,
-                                                           int* __restrict__ info) {
-  cg::cluster_group cluster = cg::this_cluster();
-  const int C = (int)cluster.num_blocks();
-  const int me = (int)cluster.block_rank();
-  extern __shared__ __align__(16) double jsm[];
-  __shared__ JacShared sh;
-  auto csync = [&]() {
-    if (C == 1) __syncthreads();
-    else cluster.sync();
-  };
-  auto remote = [&](auto* p, int cta) { return C == 1 ? p : cluster.map_shared_rank(p, cta); };
-
-  const int L = ldot + lacc;
-  const int lds = (L + 1) & ~1;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tid = threadIdx.x;
-  // slot s -> CTA s % C, local row s / C
-  auto slot_ptr = [&](int s) -> double* { return remote(jsm + (s / C) * lds, s % C); };
-  const int nslots = mode == 0 ? n : N;
-  const int myslots = (nslots - me + C - 1) / C;
-
-  // ------------------------------------------------------------- load ----
-  if (mode == 0) {  // B rows (symmetric): slot i = row i
-    for (int ls = warp; ls < myslots; ls += JAC_WARPS) {
-      const int i = ls * C + me;
-      for (int c = lane; c < lds; c += 32) jsm[ls * lds + c] = c < n ? in[(size_t)i * ldin + c] : 0.0;
-    }
-  } else {  // given columns + identity accumulator
-    for (int ls = warp; ls < myslots; ls += JAC_WARPS) {
-      const int j = ls * C + me;
-      for (int c = lane; c < lds; c += 32)
-        jsm[ls * lds + c] = c < ldot ? in[(size_t)j * ldin + c] : (c - ldot == j ? 1.0 : 0.0);
-    }
+template <int C>
+struct Cl {
+  cg::cluster_group c = cg::this_cluster();
+  __device__ int rank() const { return C == 1 ? 0 : (int)c.block_rank(); }
+  __device__ void sync() {
+    if constexpr (C == 1) __syncthreads();
+    else c.sync();
   }
-  for (int i = tid; i < JAC_MAXSLOTS; i += JAC_THREADS) sh.piv_flag[i] = 0;
-  if (tid < 3) sh.flag[tid] = 0;
-  csync();
+  template <class T>
+  __device__ T* at(T* p, int q) {
+    if constexpr (C == 1) return p;
+    else return c.map_shared_rank(p, q);
+  }
+};
 
-  int K = N;
-  if (mode == 0) {
-    // ---- max diagonal (the scale of the truncation threshold) ----
+// argmax over a warp: larger value wins, ties -> lower index (idx < 0 = none)
+__device__ __forceinline__ void warp_argmax(double& v, int& i) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, i, o);
+    if (oi >= 0 && (i < 0 || ov > v || (ov == v && oi < i))) v = ov, i = oi;
+  }
+}
+
+// Reciprocal and reciprocal square root: MUFU approximation + two Newton steps.
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double e = fma(-x * y, y, 1.0);
+    y = fma(0.5 * y, e, y);
+  }
+  return y;
+}
+
+template <int C, int G, int V>
+__global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
+  Cl<C> cl;
+  const int h = cl.rank();
+  extern __shared__ __align__(16) double dsm[];
+  __shared__ int s_order[JMAX];  // column k -> slot (EIG: pivot order)
+  __shared__ int s_rank[JMAX];
+  __shared__ double s_nrm[JMAX];
+  __shared__ double s_cand[4][2];  // C > 1: per-CTA pivot candidates (value, index)
+  __shared__ double s_red[JW];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long t_start = clock64();
+  const int nslots = a.mode == 0 ? a.n : a.N;
+  const int P = a.P, Lh = a.Lh;
+  const int row0 = h * Lh;                         // first global row held here
+  const int nloc = max(0, min(Lh, a.L - row0));    // rows held here
+  double* X = dsm;                                 // [nslots][P]
+  double* bc = X + (size_t)(nslots + 1) * P;       // [JMAX] pivot row (EIG, C > 1)
+  double* xch = bc + JMAX;                         // C > 1: [2][JMAXP][C][4] pair partials
+  double* nx = xch + (C > 1 ? 2 * JMAXP * C * 4 : 0);  // [C][JMAX] partial column norms
+
+  // ------------------------------------------------------------ load ----
+  for (int r = tid; r < P; r += JT) X[(size_t)nslots * P + r] = 0.0;  // the zero (pad) slot
+  if (a.mode == 0) {  // slot i = column i of B (= row i), rows row0..row0+Lh
+    for (int s = warp; s < nslots; s += JW)
+      for (int r = lane; r < P; r += 32)
+        X[s * P + r] = r < nloc ? a.in[(size_t)s * a.ldin + row0 + r] : 0.0;
+  } else {  // K's columns, zero rows up to dpad, then the identity accumulator
+    for (int s = warp; s < nslots; s += JW)
+      for (int r = lane; r < P; r += 32) {
+        const int gr = row0 + r;
+        double v = 0.0;
+        if (r < nloc) v = gr < a.ldot ? a.in[(size_t)s * a.ldin + gr] : (gr - a.dpad == s ? 1.0 : 0.0);
+        X[s * P + r] = v;
+      }
+  }
+  __syncthreads();
+
+  int K = nslots;
+  if (a.mode == 0) {
+    // ---- scale of the truncation: max diagonal of B ----
+    const int n = a.n;
     double dmax = 0.0;
-    for (int ls = tid; ls < myslots; ls += JAC_THREADS) dmax = fmax(dmax, jsm[ls * lds + ls * C + me]);
+    for (int i = tid; i < n; i += JT)
+      if (i >= row0 && i < row0 + nloc) dmax = fmax(dmax, X[i * P + (i - row0)]);
+#pragma unroll
     for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
-    if (lane == 0) sh.red_d[warp] = dmax;
+    if (lane == 0) s_red[warp] = dmax;
     __syncthreads();
     if (tid == 0) {
       double c = 0.0;
-      for (int w = 0; w < JAC_WARPS; ++w) c = fmax(c, sh.red_d[w]);
-      sh.cta_val[1] = c;
-      sh.k = 0;
-      sh.mu = 0.0;
+      for (int w = 0; w < JW; ++w) c = fmax(c, s_red[w]);
+      for (int q = 0; q < C; ++q) cl.at(&s_cand[0][0], q)[2 * h] = c;
     }
-    csync();
-    double dgmax = 0.0;
-    for (int q = 0; q < C; ++q) dgmax = fmax(dgmax, remote(&sh, q)->cta_val[1]);
-    const double tabs = trunc * dgmax;
-    csync();
+    cl.sync();
+    double gmax = 0.0;
+    for (int q = 0; q < C; ++q) gmax = fmax(gmax, s_cand[q][0]);
+    const double tabs = a.trunc * gmax;
+    cl.sync();
 
-    // ---- diagonally pivoted Cholesky, right-looking, truncated at tabs ----
-    for (int step = 0; step < n; ++step) {
-      // argmax of the remaining diagonal (ties -> lowest index)
+    // ---- diagonally pivoted Cholesky, right-looking, in place ----
+    // Step k with pivot p: X[:, k] := S[:, p] / sqrt(S_pp), stored in slot p
+    // (zero on rows pivoted earlier; finalised one step late, when slot p is no
+    // longer read), and S[c][c'] -= S[c][p] S[c'][p] / S_pp on the remaining
+    // block.  Pivoted rows/slots are tracked in per-thread bit masks: this
+    // thread's rows are row0 + lane + 32 j, its warp's slots are warp + JW j'.
+    // s_rank[] doubles as the "pivoted" flag per global row during this phase.
+    for (int i = tid; i < JMAX; i += JT) s_rank[i] = 0;
+    __syncthreads();
+    uint32_t rmask = 0, smask = 0;
+    int prev = -1;
+    int k = 0;
+    for (; k < n; ++k) {
+      // argmax of the remaining diagonal (ties -> lowest index), every warp redundantly
       double bv = -1.0;
       int bi = -1;
-      for (int ls = tid; ls < myslots; ls += JAC_THREADS) {
-        const int i = ls * C + me;
-        if (sh.piv_flag[ls]) continue;
-        const double d = jsm[ls * lds + i];
-        if (d > bv || (d == bv && i < bi)) bv = d, bi = i;
+      for (int j = 0; 32 * j < nloc; ++j) {
+        const int r = lane + 32 * j;
+        if (r < nloc && !((rmask >> j) & 1)) {
+          double d = X[(row0 + r) * P + r];
+          if (isnan(d)) d = INFINITY;  // non-finite input: pivot it (NaN spreads, caught downstream)
+          if (bi < 0 || d > bv) bv = d, bi = row0 + r;
+        }
       }
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov > bv || (ov == bv && oi >= 0 && (bi < 0 || oi < bi))) bv = ov, bi = oi;
+      warp_argmax(bv, bi);
+      int p = bi;
+      double dp = bv;
+      if constexpr (C > 1) {
+        if (tid == 0)
+          for (int q = 0; q < C; ++q) {
+            double* cq = cl.at(&s_cand[0][0], q);
+            cq[2 * h] = bv;
+            cq[2 * h + 1] = (double)bi;
+          }
+        cl.sync();
+        p = -1, dp = -1.0;
+        for (int q = 0; q < C; ++q) {
+          const double v = s_cand[q][0];
+          const int i = (int)s_cand[q][1];
+          if (i >= 0 && (p < 0 || v > dp || (v == dp && i < p))) dp = v, p = i;
+        }
       }
-      if (lane == 0) sh.red_d[warp] = bv, sh.red_i[warp] = bi;
-      __syncthreads();
+      if (p < 0 || !(dp > tabs)) break;  // uniform over the cluster
       if (tid == 0) {
-        double v = -1.0;
-        int ix = -1;
-        for (int w = 0; w < JAC_WARPS; ++w)
-          if (sh.red_d[w] > v || (sh.red_d[w] == v && sh.red_i[w] >= 0 && (ix < 0 || sh.red_i[w] < ix)))
-            v = sh.red_d[w], ix = sh.red_i[w];
-        sh.cta_val[0] = v;
-        sh.cta_idx = ix;
+        s_order[k] = p;
+        s_rank[p] = 1;
+        s_nrm[k] = 1.0 / sqrt(dp);
       }
-      csync();
-      double v = -1.0;
-      int j = -1;
-      for (int q = 0; q < C; ++q) {
-        JacShared* o = remote(&sh, q);
-        const double ov = o->cta_val[0];
-        const int oi = o->cta_idx;
-        if (ov > v || (ov == v && oi >= 0 && (j < 0 || oi < j))) v = ov, j = oi;
+      const double inv = 1.0 / dp;
+      const double* fsrc = X + p * P;  // C == 1: S[s][p] = slot p, row s
+      if constexpr (C > 1) {
+        // the owner of row p broadcasts S[p][s] (row p of every slot) to the cluster
+        if (p >= row0 && p < row0 + nloc)
+          for (int s = tid; s < n; s += JT) {
+            const double v = X[s * P + (p - row0)];
+            for (int q = 0; q < C; ++q) cl.at(bc, q)[s] = v;
+          }
+        cl.sync();
+        fsrc = bc;
       }
-      if (j < 0 || !(v > tabs)) break;  // uniform across the cluster
-      // pivot row r = S[j,:] / sqrt(S_jj): copy into every CTA's bcast buffer
-      const double* pr = slot_ptr(j);
-      const double inv = 1.0 / sqrt(v);
-      for (int c = tid; c < n; c += JAC_THREADS) sh.bcast[c] = pr[c] * inv;
-      csync();  // all copies done before the owner overwrites its row
-      if ((j % C) == me) {
-        const int ls = j / C;
-        for (int c = tid; c < lds; c += JAC_THREADS) jsm[ls * lds + c] = c < n ? sh.bcast[c] : 0.0;
-        if (tid == 0) sh.piv_flag[ls] = 1;
+      // rank-1 update of the remaining block (slots of this warp, rows of this lane);
+      // the pivot column is held in registers, zero on excluded rows (no-op FMA)
+      const double* xp = X + p * P;
+      double pv[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int r = lane + 32 * j;
+        pv[j] = (r < nloc && row0 + r != p && !((rmask >> j) & 1)) ? xp[r] : 0.0;
       }
-      if (tid == 0) sh.order[step] = j;
-      // rank-1 update of the remaining rows: S[i][c] -= r_i r_c
-      for (int e = tid; e < myslots * n; e += JAC_THREADS) {
-        const int ls = e / n, c = e % n;
-        const int i = ls * C + me;
-        if (i == j || sh.piv_flag[ls]) continue;
-        jsm[ls * lds + c] -= sh.bcast[i] * sh.bcast[c];
+      for (int jj = 0; warp + JW * jj < n; ++jj) {
+        const int s = warp + JW * jj;
+        if (s == p || ((smask >> jj) & 1)) continue;
+        const double f = fsrc[s] * inv;
+        double* xs = X + s * P;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int r = lane + 32 * j;
+          if (32 * j < nloc && r < nloc) xs[r] = fma(-pv[j], f, xs[r]);
+        }
       }
-      if (tid == 0) sh.k = step + 1;
-      csync();
+      // finalise the previous pivot's column: zero on rows pivoted before it, scaled elsewhere
+      if (prev >= 0) {
+        const double rsq = s_nrm[k - 1];
+        double* xs = X + prev * P;
+        for (int e = tid; e < nloc; e += JT) {
+          const int gr = row0 + e;
+          const bool dead = s_rank[gr] != 0 && gr != prev && gr != p;
+          xs[e] = dead ? 0.0 : xs[e] * rsq;
+        }
+      }
+      if (p >= row0 && p < row0 + nloc && ((p - row0) & 31) == lane) rmask |= 1u << ((p - row0) >> 5);
+      if ((p % JW) == warp) smask |= 1u << (p / JW);
+      prev = p;
+      __syncthreads();  // (C > 1: the cluster barriers above order the DSMEM traffic)
     }
-    K = sh.k;
+    K = k;
+    if (prev >= 0) {
+      const double rsq = s_nrm[K - 1];
+      double* xs = X + prev * P;
+      for (int e = tid; e < nloc; e += JT) {
+        const int gr = row0 + e;
+        const bool dead = s_rank[gr] != 0 && gr != prev;
+        xs[e] = dead ? 0.0 : xs[e] * rsq;
+      }
+    }
   } else {
-    for (int i = tid; i < N; i += JAC_THREADS) sh.order[i] = i;
-    if (tid == 0) sh.mu = 0.0;
-    __syncthreads();
+    for (int i = tid; i < nslots; i += JT) s_order[i] = i;
   }
-  // nu2 = max squared column norm (for the noise-pair skip test)
-  {
-    double mx = 0.0;
-    for (int jj = warp; jj < K; jj += JAC_WARPS) {
-      const int s = sh.order[jj];
-      if (s % C != me) continue;
-      const double* x = jsm + (s / C) * lds;
-      double a = 0.0;
-      for (int c = lane; c < ldot; c += 32) a = fma(x[c], x[c], a);
-      mx = fmax(mx, warp_sum_bcast(a));
+  cl.sync();
+
+  // ---- column norms^2 over the dot rows (partial per CTA, summed in CTA order) ----
+  auto col_norms = [&](int ncols) {
+    const int dloc = max(0, min(nloc, a.dpad - row0));
+    for (int kk = warp; kk < ncols; kk += JW) {
+      const double* x = X + s_order[kk] * P;
+      double s = 0.0;
+      for (int r = lane; r < dloc; r += 32) s = fma(x[r], x[r], s);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0)
+        for (int q = 0; q < C; ++q) cl.at(nx, q)[h * JMAX + kk] = s;
     }
-    if (lane == 0) sh.red_d[warp] = mx;
+    cl.sync();
+    for (int kk = tid; kk < ncols; kk += JT) {
+      double s = 0.0;
+      for (int q = 0; q < C; ++q) s += nx[q * JMAX + kk];
+      s_nrm[kk] = s;
+    }
     __syncthreads();
-    if (tid == 0) {
-      double a = 0.0;
-      for (int w = 0; w < JAC_WARPS; ++w) a = fmax(a, sh.red_d[w]);
-      sh.cta_val[1] = a;
-    }
-    csync();
-    double a = 0.0;
-    for (int q = 0; q < C; ++q) a = fmax(a, remote(&sh, q)->cta_val[1]);
-    sh.nu2 = a;  // identical on every CTA
-  }
-  csync();
+  };
+
+  col_norms(K);
+  double nu2 = 0.0;
+  for (int kk = 0; kk < K; ++kk) nu2 = fmax(nu2, s_nrm[kk]);
+  const double skip2 = (kEps * kEps) * nu2;
+  const double tol2 = a.tol * a.tol;
+  cl.sync();  // s_nrm reads done before it is reused
 
   // ---------------------------------------------------- Jacobi sweeps ----
-  const int NE = K + (K & 1);
-  constexpr int GPW = 32 / G;  // pair groups per warp
+  // Circle (round-robin) ordering on positions 0..NE-1: in round r, pair i is
+  // (p, q) = (i ? 1 + (i-1+r) mod (NE-1) : 0, 1 + (NE-2-i+r) mod (NE-1)),
+  // advanced incrementally.  An odd K is padded with the all-zero slot
+  // `nslots` (it never rotates: its dot products are 0).  Pair i is handled by
+  // group i % GPW of warp i / GPW (the launcher guarantees one pass).
+  const long long t_chol = clock64();
+  const int NE = K + (K & 1), npairs = NE / 2;
+  if (K & 1) s_order[K] = nslots;
+  __syncthreads();
+  constexpr int GPW = 32 / G;
   const int grp = lane / G, gl = lane % G;
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
-  const int gw = (me * JAC_WARPS + warp) * GPW + grp;
-  const int tg = C * JAC_WARPS * GPW;
-  const double skip2 = (kEps * kEps) * sh.nu2;
-  int sweep = 0;
+  const int gidx = warp * GPW + grp;
+  const bool has = gidx < npairs;
+  // rows of this lane: 2*gl + 2*G*e (+0, +1), e < V (storage padded with zeros);
+  // only rows below dpad (SVD: the matrix part) enter the dot products
+  const int dloc = max(0, min(nloc, a.dpad - row0));
+  const int elim = dloc > 2 * gl ? (dloc - 2 * gl + 2 * G - 1) / (2 * G) : 0;
+  int pos_p = gidx, pos_q = NE - 1 - gidx;  // round 0 (gidx == 0 -> fixed position 0)
+  int sweep = 0, rounds = 0;
   bool converged = K <= 1;
-  for (; sweep < max_sweeps && !converged; ++sweep) {
-    if (tid == 0) sh.flag[(sweep + 1) % 3] = 0;
-    for (int r = 0; r < NE - 1; ++r) {
-      for (int i = gw; i < NE / 2; i += tg) {
-        const int pp = i, qq = NE - 1 - i;
-        const int p = pp == 0 ? 0 : 1 + (pp - 1 + r) % (NE - 1);
-        const int q = 1 + (qq - 1 + r) % (NE - 1);
-        if (p >= K || q >= K) continue;  // the pad column of an odd K
-        double* xp = slot_ptr(sh.order[p]);
-        double* xq = slot_ptr(sh.order[q]);
-        double vp[EPG], vq[EPG];
-        double al = 0.0, be = 0.0, ga = 0.0;
+  for (; sweep < a.max_sweeps && !converged; ++sweep) {
+    int any = 0;
+    for (int r = 0; r < NE - 1; ++r, ++rounds) {
+      int rot = 0;
+      double al = 0.0, be = 0.0, ga = 0.0;
+      double2 vp[V], vq[V];
+      double2* xp = nullptr;
+      double2* xq = nullptr;
+      if (has) {
+        xp = reinterpret_cast<double2*>(X + s_order[pos_p] * P) + gl;
+        xq = reinterpret_cast<double2*>(X + s_order[pos_q] * P) + gl;
 #pragma unroll
-        for (int e = 0; e < EPG; ++e) {
-          const int idx = gl + G * e;
-          vp[e] = idx < L ? xp[idx] : 0.0;
-          vq[e] = idx < L ? xq[idx] : 0.0;
-          if (idx < ldot) {
-            al = fma(vp[e], vp[e], al);
-            be = fma(vq[e], vq[e], be);
-            ga = fma(vp[e], vq[e], ga);
+        for (int e = 0; e < V; ++e) vp[e] = xp[G * e], vq[e] = xq[G * e];  // all loads in flight
+        double al1 = 0.0, be1 = 0.0, ga1 = 0.0;
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          if (e < elim) {
+            al = fma(vp[e].x, vp[e].x, al);
+            al1 = fma(vp[e].y, vp[e].y, al1);
+            be = fma(vq[e].x, vq[e].x, be);
+            be1 = fma(vq[e].y, vq[e].y, be1);
+            ga = fma(vp[e].x, vq[e].x, ga);
+            ga1 = fma(vp[e].y, vq[e].y, ga1);
           }
         }
+        al += al1;
+        be += be1;
+        ga += ga1;
 #pragma unroll
-        for (int o = G / 2; o > 0; o >>= 1) {
+        for (int o = G / 2; o > 0; o >>= 1) {  // xor butterfly: identical sums in every lane
           al += __shfl_xor_sync(gmask, al, o);
           be += __shfl_xor_sync(gmask, be, o);
           ga += __shfl_xor_sync(gmask, ga, o);
         }
-        const int src = grp * G;
-        al = __shfl_sync(gmask, al, src);
-        be = __shfl_sync(gmask, be, src);
-        ga = __shfl_sync(gmask, ga, src);
-        if (ga != 0.0 && ga * ga > tol * tol * al * be && fmax(al, be) > skip2) {
-          const double zeta = (be - al) / (2.0 * ga);
-          const double tt = copysign(1.0, zeta) / (fabs(zeta) + hypot(1.0, zeta));
-          const double c = 1.0 / sqrt(fma(tt, tt, 1.0));
-          const double s = c * tt;
-#pragma unroll
-          for (int e = 0; e < EPG; ++e) {
-            const int idx = gl + G * e;
-            if (idx < L) {
-              xp[idx] = c * vp[e] - s * vq[e];
-              xq[idx] = s * vp[e] + c * vq[e];
-            }
-          }
-          if (gl == 0) sh.flag[sweep % 3] = 1;
-        }
       }
-      csync();
+      if constexpr (C > 1) {
+        double* xb = xch + ((size_t)(rounds & 1) * JMAXP + (has ? gidx : 0)) * C * 4;
+        if (has && gl == 0)
+          for (int qc = 0; qc < C; ++qc) {
+            double* d = cl.at(xb, qc) + h * 4;
+            d[0] = al;
+            d[1] = be;
+            d[2] = ga;
+          }
+        cl.sync();
+        al = be = ga = 0.0;
+        for (int qc = 0; qc < C; ++qc) al += xb[qc * 4], be += xb[qc * 4 + 1], ga += xb[qc * 4 + 2];
+      }
+      if (has && ga != 0.0 && ga * ga > tol2 * al * be && fmax(al, be) > skip2) {
+        // rotation zeroing the (p, q) entry of [[al, ga], [ga, be]], d = be - al:
+        //   t = tan(theta) = sign(d) 2ga / (|d| + sqrt(d^2 + 4ga^2)),  c = 1/sqrt(1+t^2), s = c t.
+        // d and 2ga are first scaled by a power of two (exact) so the squares cannot
+        // over/underflow; reciprocal / rsqrt by MUFU + two Newton steps (~1 ulp).
+        double d = be - al, g2 = ga + ga;
+        const double big = fmax(fabs(d), fabs(g2));
+        const int ex = (int)((__double_as_longlong(big) >> 52) & 0x7ff);  // biased exponent
+        const double sc = __longlong_as_double((long long)(2046 - ex) << 52);  // 2^(1023 - ex + 0)
+        d *= sc;
+        g2 *= sc;
+        const double w = fma(d, d, g2 * g2);
+        const double root = w * rsqrt_nr(w);
+        const double t = (d >= 0.0 ? g2 : -g2) * rcp_nr(fabs(d) + root);
+        const double c = rsqrt_nr(fma(t, t, 1.0));
+        const double sn = c * t;
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          xp[G * e] = make_double2(fma(c, vp[e].x, -sn * vq[e].x), fma(c, vp[e].y, -sn * vq[e].y));
+          xq[G * e] = make_double2(fma(sn, vp[e].x, c * vq[e].x), fma(sn, vp[e].y, c * vq[e].y));
+        }
+        rot = 1;
+      }
+      // advance this pair's positions to the next round
+      if (pos_p != 0) pos_p = pos_p == NE - 1 ? 1 : pos_p + 1;
+      pos_q = pos_q == NE - 1 ? 1 : pos_q + 1;
+      any |= __syncthreads_or(rot);
     }
-    int any = 0;
-    for (int q = 0; q < C; ++q) any |= remote(&sh, q)->flag[sweep % 3];
     converged = !any;
   }
 
+  const long long t_sweeps = clock64();
   // ------------------------------------------ norms, order, write back ----
-  for (int jj = warp; jj < K; jj += JAC_WARPS) {
-    const int s = sh.order[jj];
-    if (s % C != me) continue;
-    const double* x = jsm + (s / C) * lds;
-    double a = 0.0;
-    for (int c = lane; c < ldot; c += 32) a = fma(x[c], x[c], a);
-    a = warp_sum_bcast(a);
-    if (lane == 0) sh.nrm[jj] = sqrt(a);  // indexed by column (jj), stored where the slot lives
-  }
-  csync();
-  for (int jj = tid; jj < K; jj += JAC_THREADS) {
-    const int s = sh.order[jj];
-    if (s % C != me) continue;
-    const double nj = sh.nrm[jj];
+  col_norms(K);
+  for (int kk = tid; kk < K; kk += JT) {
+    const double nj = s_nrm[kk];
     int rk = 0;
     for (int ii = 0; ii < K; ++ii) {
-      const double ni = remote(&sh, sh.order[ii] % C)->nrm[ii];
-      rk += (ni > nj) || (ni == nj && ii < jj);
+      const double ni = s_nrm[ii];
+      rk += (ni > nj) || (ni == nj && ii < kk);
     }
-    sh.rank_out[jj] = rk;
+    s_rank[kk] = rk;
   }
   __syncthreads();
-  const double mu = sh.mu;
-  for (int jj = warp; jj < K; jj += JAC_WARPS) {
-    const int s = sh.order[jj];
-    if (s % C != me) continue;
-    const int rk = sh.rank_out[jj];
-    const double nj = sh.nrm[jj];
+  // output column rk: first ldot rows normalised, then the accumulator rows (SVD)
+  for (int kk = warp; kk < K; kk += JW) {
+    const int rk = s_rank[kk];
+    const double n2 = s_nrm[kk];
+    const double nj = sqrt(n2);
     const double invn = nj > 0.0 ? 1.0 / nj : 0.0;
-    const double* x = jsm + (s / C) * lds;
-    double* dst = out + (size_t)rk * ldout;
-    for (int c = lane; c < L; c += 32) dst[c] = c < ldot ? x[c] * invn : x[c];
-    if (lane == 0) vals[rk] = mode == 0 ? fma(nj, nj, mu) : nj;
+    const double* x = X + s_order[kk] * P;
+    double* dst = a.out + (size_t)rk * a.ldout;
+    for (int r = lane; r < nloc; r += 32) {
+      const int gr = row0 + r;
+      if (gr < a.ldot) dst[gr] = x[r] * invn;
+      else if (gr >= a.dpad) dst[a.ldot + (gr - a.dpad)] = x[r];
+    }
+    if (lane == 0 && h == 0) a.vals[rk] = a.mode == 0 ? n2 : nj;
   }
-  if (me == 0 && tid == 0) {
-    info[0] = sweep;
-    info[1] = converged ? 1 : 0;
-    info[2] = K;
+  if (h == 0 && tid == 0) {
+    a.info[0] = sweep;
+    a.info[1] = converged ? 1 : 0;
+    a.info[2] = K;
+    a.info[3] = (int)((t_chol - t_start) >> 4);  // phase timings, units of 16 cycles
+    a.info[4] = (int)((t_sweeps - t_chol) >> 4);
+    a.info[5] = rounds;
   }
-  cluster.sync();  // keep DSMEM alive until every CTA is done reading it
+  if constexpr (C > 1) cl.sync();  // keep DSMEM alive until every CTA is done with it
 }
 
-template <int G, int EPG>
-static cudaError_t jac_go(int C, size_t smem, const double* in, int ldin, int mode, int n, int N,
-                          int ldot, int lacc, double tol, double trunc, int max_sweeps,
-                          double* out, int ldout, double* vals, int* info, cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute(jacobi_kernel<G, EPG>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+// ------------------------------------------------------------- launch ----
+template <int C, int G, int V>
+static cudaError_t jac_go(const JacArgs& a, size_t smem, cudaStream_t s) {
+  auto kern = jacobi_kernel<C, G, V>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(C);
-  cfg.blockDim = dim3(JAC_THREADS);
+  cfg.blockDim = dim3(JT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -335,45 +468,123 @@ static cudaError_t jac_go(int C, size_t smem, const double* in, int ldin, int mo
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, jacobi_kernel<G, EPG>, in, ldin, mode, n, N, ldot, lacc, tol,
-                            trunc, max_sweeps, out, ldout, vals, info);
+  return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-static cudaError_t jac_dispatch(int mode, const double* in, int ldin, int n, int N, int ldot,
-                                int lacc, double tol, double trunc, int max_sweeps, double* out,
-                                int ldout, double* vals, int* info, cudaStream_t s) {
-  const int L = ldot + lacc;
-  const int nslots = mode == 0 ? n : N;
+template <int C, int G>
+static cudaError_t jac_v(const JacArgs& a, size_t smem, cudaStream_t s) {
+  switch (a.V) {
+    case 2: return jac_go<C, G, 2>(a, smem, s);
+    case 4: return jac_go<C, G, 4>(a, smem, s);
+    case 6: return jac_go<C, G, 6>(a, smem, s);
+    default: return jac_go<C, G, 8>(a, smem, s);
+  }
+}
+
+template <int C>
+static cudaError_t jac_g(const JacArgs& a, int g, size_t smem, cudaStream_t s) {
+  switch (g) {
+    case 4: return jac_v<C, 4>(a, smem, s);
+    case 8: return jac_v<C, 8>(a, smem, s);
+    default: return jac_v<C, 16>(a, smem, s);
+  }
+}
+
+static size_t jac_smem(int C, int nslots, int P) {
+  return ((size_t)(nslots + 1) * P + JMAX + (C > 1 ? 2 * JMAXP * C * 4 : 0) + (size_t)C * JMAX) * 8;
+}
+
+// Round cost model (cycles; B200 measured: DFMA/DADD 7-cycle latency, 2 issue
+// cycles per warp-instruction on the 16-lane FP64 unit, SHFL+DADD 35, LDS 29,
+// MUFU f64 ~19; the rotation parameters ~230 on the critical path; a cluster
+// exchange + barrier ~600).
+static double jac_round_cost(int C, int G, int V, int npairs) {
+  const int gpw = 32 / G;
+  const int warps = (int)ceil_div(npairs, gpw);
+  const int per_smsp = (int)ceil_div(warps, 4);
+  int lg = 0;
+  while ((1 << lg) < G) ++lg;
+  const double pipe = 2.0 * per_smsp * (14.0 * V + 3.0 * lg + 35.0) + 8.0 * per_smsp * V;
+  const double chain = 60.0 + 2.0 * V + 7.0 * V + 35.0 * lg + 230.0 + 16.0 * V;
+  return std::max(pipe, chain) + (C > 1 ? 600.0 : 50.0);
+}
+
+static cudaError_t jac_dispatch(JacArgs a, cudaStream_t s) {
+  const int nslots = a.mode == 0 ? a.n : a.N;
   if (nslots <= 0) return cudaSuccess;
-  if (L > 512 || nslots > 512) return cudaErrorInvalidValue;
-  const int lds = (L + 1) & ~1;
-  const size_t budget = std::min<size_t>(dev_info().smem_optin - 16384, 200 * 1024);
-  int C = 1;
-  while (C < 8 && ((size_t)((nslots + C - 1) / C) * lds * 8 > budget ||
-                   (nslots + C - 1) / C > JAC_MAXSLOTS))
-    C *= 2;
-  const size_t smem = (size_t)((nslots + C - 1) / C) * lds * 8;
-  if (smem > budget) return cudaErrorInvalidValue;
-#define JGO(G, E) \
-  return jac_go<G, E>(C, smem, in, ldin, mode, n, N, ldot, lacc, tol, trunc, max_sweeps, out, ldout, vals, info, s)
-  if (L <= 32) JGO(8, 4);
-  if (L <= 64) JGO(8, 8);
-  if (L <= 128) JGO(8, 16);
-  if (L <= 256) JGO(16, 16);
-  JGO(32, 16);
-#undef JGO
+  if (nslots > JMAX || a.L > 2 * JMAX) return cudaErrorInvalidValue;
+  const size_t budget = dev_info().smem_optin - 8 * 1024;  // static shared + slack
+  const int npairs = (nslots + 1) / 2;
+  // tuning overrides (experiments only): TSSVD_JAC_G, TSSVD_JAC_C
+  static const int force_g = getenv("TSSVD_JAC_G") ? atoi(getenv("TSSVD_JAC_G")) : 0;
+  static const int force_c = getenv("TSSVD_JAC_C") ? atoi(getenv("TSSVD_JAC_C")) : 0;
+  double best = 1e300;
+  int bC = 0, bG = 0, bV = 0, bLh = 0;
+  for (int C = 1; C <= 4; C *= 2) {
+    const int Lh = (int)((ceil_div(a.L, C) + 1) & ~1);
+    for (int G = 4; G <= 16; G *= 2) {
+      if (JW * (32 / G) < npairs) continue;  // one pass over the pairs
+      if ((force_g && G != force_g) || (force_c && C != force_c)) continue;
+      int V = (int)ceil_div(Lh, 2 * G);
+      if (V > 8) continue;
+      V = V <= 2 ? 2 : (V + 1) & ~1;  // instantiated: 2, 4, 6, 8
+      if (jac_smem(C, nslots, 2 * G * V) > budget) continue;
+      const double cost = jac_round_cost(C, G, V, npairs);
+      if (cost < best) best = cost, bC = C, bG = G, bV = V, bLh = Lh;
+    }
+  }
+  if (!bC) return cudaErrorInvalidValue;
+  a.Lh = bLh;
+  a.V = bV;
+  a.P = 2 * bG * bV;
+  const size_t smem = jac_smem(bC, nslots, a.P);
+  if (bC == 1) return jac_g<1>(a, bG, smem, s);
+  if (bC == 2) return jac_g<2>(a, bG, smem, s);
+  return jac_g<4>(a, bG, smem, s);
 }
 
 cudaError_t launch_jacobi_eig(const double* B, int ldb, int n, double tol, double trunc,
                               int max_sweeps, double* vecs, int ldv, double* vals, int* info,
                               cudaStream_t s) {
-  return jac_dispatch(0, B, ldb, n, n, n, 0, tol, trunc, max_sweeps, vecs, ldv, vals, info, s);
+  JacArgs a{};
+  a.in = B;
+  a.ldin = ldb;
+  a.mode = 0;
+  a.n = n;
+  a.N = 0;
+  a.ldot = n;
+  a.dpad = n;
+  a.L = n;
+  a.tol = tol;
+  a.trunc = trunc;
+  a.max_sweeps = max_sweeps;
+  a.out = vecs;
+  a.ldout = ldv;
+  a.vals = vals;
+  a.info = info;
+  return jac_dispatch(a, s);
 }
 
 cudaError_t launch_jacobi_svd(const double* cols, int ldc, int N, int ldot, double tol,
                               int max_sweeps, double* out, int ldout, double* vals, int* info,
                               cudaStream_t s) {
-  return jac_dispatch(1, cols, ldc, 0, N, ldot, N, tol, 0.0, max_sweeps, out, ldout, vals, info, s);
+  JacArgs a{};
+  a.in = cols;
+  a.ldin = ldc;
+  a.mode = 1;
+  a.n = 0;
+  a.N = N;
+  a.ldot = ldot;
+  a.dpad = (ldot + 1) & ~1;
+  a.L = a.dpad + N;
+  a.tol = tol;
+  a.trunc = 0.0;
+  a.max_sweeps = max_sweeps;
+  a.out = out;
+  a.ldout = ldout;
+  a.vals = vals;
+  a.info = info;
+  return jac_dispatch(a, s);
 }
 
 }  // namespace tsk
