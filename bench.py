@@ -233,7 +233,7 @@ def run_ours(args, rank, world, local_rank):
         e2e = {"value": round(total_a_bytes / (te.item() * 1e-3) / 1e9, 3), "unit": "GB/s",
                "ms_per_step": round(te.item(), 3),
                "h2d_bytes_per_step": int(8 * m_local * n),
-               "d2h_bytes_per_step": int(8 * (m_local * r + r + n * r))}
+               "d2h_bytes_per_step": int(8 * (m_local * ((r + 1) & ~1) + r + n * r))}
 
     # roofline of the dominant kernel (largest share of the step's device time)
     shares = {k: sum(v) / args.steps for k, v in pass_ms.items()}

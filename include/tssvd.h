@@ -92,6 +92,9 @@ void tssvd_opts_default(tssvd_opts* opts);
  *   U        m_local x n capacity, ldu >= n, ldu even, 16-byte aligned: columns
  *            [0, r) receive U_p (sharded like A); the rest is scratch.
  *            U may alias A (same pointer and ldu == lda): then A is overwritten.
+ *            host_io == 1: U is a host buffer of m_local x n doubles; ldu >= n
+ *            gives row-major U with that leading dimension, ldu == 0 returns U
+ *            PACKED with leading dimension (r + 1) & ~1 (one contiguous D2H copy).
  *   sigma    n capacity, [0, r) written, replicated on every rank
  *   V        n x n capacity, ldv >= n: columns [0, r) written, replicated
  *   rank     HOST out: r (identical on every rank)

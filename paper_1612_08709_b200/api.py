@@ -103,16 +103,21 @@ def tssvd(A: torch.Tensor, wp: float = 1e-11, passes: int = 2, comm: Comm | None
     check(lib().tssvd_workspace_size(cptr, m, n, ctypes.byref(opts), ctypes.byref(nbytes)))
     ws = _workspace(nbytes.value, dev)
     pin = host and torch.cuda.is_available()
+    packed = host and U is None  # host_io: U comes back packed (ld (r+1)&~1), one D2H copy
     if U is None:
         U = A if (inplace and not host) else torch.empty((m, n), dtype=torch.float64,
                                                          device=A.device, pin_memory=pin)
     sigma = torch.empty(n, dtype=torch.float64, device=A.device, pin_memory=pin)
     V = torch.empty((n, n), dtype=torch.float64, device=A.device, pin_memory=pin)
     r = ctypes.c_int64()
+    ldu = 0 if packed else (U.stride(0) if m > 0 else n)
     check(lib().tssvd(cptr, _stream(dev), m, n, A.data_ptr(), lda, ctypes.byref(opts),
-                      U.data_ptr(), U.stride(0) if m > 0 else n, sigma.data_ptr(), V.data_ptr(), n,
+                      U.data_ptr(), ldu, sigma.data_ptr(), V.data_ptr(), n,
                       ctypes.byref(r), ws.data_ptr(), ws.numel()))
     k = r.value
+    if packed:
+        rp = (k + 1) & ~1
+        U = U.view(-1)[:m * rp].view(m, rp)
     return U[:, :k], sigma[:k], V[:, :k]
 
 

@@ -180,7 +180,7 @@ struct Core {
     part = a.get<double>(np);
     size_t nn = 0;
     for (int q = 1; q <= w; ++q)
-      nn = std::max(nn, (size_t)gemm_nn_grid(std::max<int64_t>(m, 1), q) * pad8(q));
+      nn = std::max(nn, (size_t)gemm_nn_grid(std::max<int64_t>(m, 1), q) * gemm_nn_part_stride(q));
     npart = a.get<double>(nn);
     B = a.get<double>((size_t)w * w);
     lam = a.get<double>(w);
@@ -229,7 +229,9 @@ void note_rank(int64_t r) {
 // otherwise).  U (m_local x w capacity, ldu) receives U[:, :r]; may alias X.
 // sigma[:r], V (w x r, ldv) replicated.  Returns r.
 int64_t core(Ctx& c, Core& b, const double* X, int64_t ldx, int64_t m_local, int w, int passes,
-             bool dist, double* U, int64_t ldu, double* sigma, double* V, int64_t ldv) {
+             bool dist, double* U, int64_t ldu, double* sigma, double* V, int64_t ldv,
+             double* Upack = nullptr) {
+  // Upack: the final U is written there packed, leading dimension (r + 1) & ~1, instead of in place
   cudaStream_t s = c.s;
   Ctx cd = c;
   if (!dist) cd.comm = nullptr;
@@ -257,7 +259,7 @@ int64_t core(Ctx& c, Core& b, const double* X, int64_t ldx, int64_t m_local, int
   {
     Pass t(s, TSSVD_PASS_XV, 2.0 * m_local * w * k, 8.0 * m_local * (w + k));
     KL(launch_gemm_nn(X, ldx, m_local, w, b.M, k, U, ldu, b.npart, s));
-    KL(launch_reduce_parts(b.npart, gemm_nn_grid(std::max<int64_t>(m_local, 1), k), pad8(k), k, b.nsq, s));
+    KL(launch_reduce_parts(b.npart, gemm_nn_grid(std::max<int64_t>(m_local, 1), k), gemm_nn_part_stride(k), k, b.nsq, s));
   }
   ++g_stats.a_passes;
   allreduce(cd, b.nsq, k);
@@ -277,7 +279,8 @@ int64_t core(Ctx& c, Core& b, const double* X, int64_t ldx, int64_t m_local, int
     KS(alg3_out(b.sig, b.idx, r, b.B, w, b.M, ldm, sigma, V, ldv, s));
     {
       Pass t(s, TSSVD_PASS_UOUT, 2.0 * m_local * nc * r, 8.0 * m_local * (nc + r));
-      KL(launch_gemm_nn(U, ldu, m_local, nc, b.M, r, U, ldu, nullptr, s));
+      KL(launch_gemm_nn(U, ldu, m_local, nc, b.M, r, Upack ? Upack : U, Upack ? (r + 1) & ~1 : ldu,
+                        nullptr, s));
     }
     return r;
   }
@@ -302,7 +305,7 @@ int64_t core(Ctx& c, Core& b, const double* X, int64_t ldx, int64_t m_local, int
   {
     Pass t(s, TSSVD_PASS_QNORM, 2.0 * m_local * nc * kz, 8.0 * m_local * nc);
     KL(launch_gemm_nn(U, ldu, m_local, nc, b.M, kz, nullptr, 0, b.npart, s));
-    KL(launch_reduce_parts(b.npart, gemm_nn_grid(std::max<int64_t>(m_local, 1), kz), pad8(kz), kz, b.tsq, s));
+    KL(launch_reduce_parts(b.npart, gemm_nn_grid(std::max<int64_t>(m_local, 1), kz), gemm_nn_part_stride(kz), kz, b.tsq, s));
   }
   allreduce(cd, b.tsq, kz);
   // Step 11: discard T below max(T) sqrt(wp).
@@ -328,7 +331,8 @@ int64_t core(Ctx& c, Core& b, const double* X, int64_t ldx, int64_t m_local, int
   KS(build_m2(b.Z, r, b.idx, b.sig, b.T, b.idx2, r2, b.Ps, b.M, ldm_r2, s));
   {
     Pass t(s, TSSVD_PASS_UOUT, 2.0 * m_local * nc * r2, 8.0 * m_local * (nc + r2));
-    KL(launch_gemm_nn(U, ldu, m_local, nc, b.M, r2, U, ldu, nullptr, s));
+    KL(launch_gemm_nn(U, ldu, m_local, nc, b.M, r2, Upack ? Upack : U, Upack ? (r2 + 1) & ~1 : ldu,
+                      nullptr, s));
   }
   return r2;
 }
@@ -364,7 +368,8 @@ int64_t global_rows(Ctx& c, int64_t m_local, void* scratch_dev) {
 struct TsPlan {
   Core core;
   int64_t* m_scratch;
-  double* a_stage;  // host_io: device copy of A (also holds U)
+  double* a_stage;  // host_io: device copy of A (also holds Y~)
+  double* u_pack;   // host_io: U packed (ld (r+1)&~1) for one contiguous D2H copy
   double* sig_stage;
   double* v_stage;
 };
@@ -374,6 +379,7 @@ size_t plan_tssvd(Arena& a, TsPlan& p, int64_t m_local, int n, const tssvd_opts*
   p.core.alloc(a, m_local, n);
   if (o && o->host_io) {
     p.a_stage = a.get<double>((size_t)std::max<int64_t>(m_local, 1) * n);
+    p.u_pack = a.get<double>((size_t)std::max<int64_t>(m_local, 1) * ((n + 1) & ~1));
     p.sig_stage = a.get<double>(n);
     p.v_stage = a.get<double>((size_t)n * n);
   }
@@ -401,8 +407,8 @@ void tssvd_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, cons
   if (!hio) {
     if (ldu < n || (ldu & 1)) fail(TSSVD_EINVAL, "ldu must be even and >= n");
     if ((m_local > 0 && (!aligned16(A) || !aligned16(U)))) fail(TSSVD_EINVAL, "A and U must be 16-byte aligned");
-  } else if (ldu < n) {
-    fail(TSSVD_EINVAL, "ldu < n");
+  } else if (ldu != 0 && ldu < n) {
+    fail(TSSVD_EINVAL, "ldu must be 0 (packed) or >= n");
   }
   if (!ws || !aligned16(ws)) fail(TSSVD_EINVAL, "workspace NULL or misaligned");
   set_device(comm);
@@ -427,8 +433,10 @@ void tssvd_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, cons
   double* Vd = V;
   int64_t ldvd = ldv;
   if (hio) {  // stage host A into the workspace (it becomes the in-place U buffer)
-    if (m_local > 0)
-      CU(cudaMemcpy2DAsync(p.a_stage, n * 8, A, lda * 8, n * 8, m_local, cudaMemcpyHostToDevice, c.s));
+    if (m_local > 0) {
+      if (lda == n) CU(cudaMemcpyAsync(p.a_stage, A, (size_t)m_local * n * 8, cudaMemcpyHostToDevice, c.s));
+      else CU(cudaMemcpy2DAsync(p.a_stage, n * 8, A, lda * 8, n * 8, m_local, cudaMemcpyHostToDevice, c.s));
+    }
     X = p.a_stage;
     ldx = n;
     Ud = p.a_stage;
@@ -437,11 +445,16 @@ void tssvd_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, cons
     Vd = p.v_stage;
     ldvd = n;
   }
+  const bool packed = hio && ldu == 0;
   const int64_t r = core(c, p.core, X, ldx, m_local, (int)n, opts->orthonormalizations, true, Ud,
-                         ldud, sigd, Vd, ldvd);
+                         ldud, sigd, Vd, ldvd, packed ? p.u_pack : nullptr);
   if (hio && r > 0) {
-    if (m_local > 0)
-      CU(cudaMemcpy2DAsync(U, ldu * 8, Ud, ldud * 8, r * 8, m_local, cudaMemcpyDeviceToHost, c.s));
+    if (m_local > 0) {
+      if (packed)  // one contiguous copy: U with leading dimension (r + 1) & ~1
+        CU(cudaMemcpyAsync(U, p.u_pack, (size_t)m_local * ((r + 1) & ~1) * 8, cudaMemcpyDeviceToHost, c.s));
+      else
+        CU(cudaMemcpy2DAsync(U, ldu * 8, Ud, ldud * 8, r * 8, m_local, cudaMemcpyDeviceToHost, c.s));
+    }
     CU(cudaMemcpyAsync(sigma, sigd, r * 8, cudaMemcpyDeviceToHost, c.s));
     CU(cudaMemcpy2DAsync(V, ldv * 8, Vd, ldvd * 8, r * 8, n, cudaMemcpyDeviceToHost, c.s));
   }
@@ -765,7 +778,7 @@ int tssvd_gram(void* stream, int64_t m, int64_t n, const double* X, int64_t ldx,
 }
 
 size_t tssvd_matmul_workspace(int64_t m, int64_t k, int64_t c) {
-  return (gemm_nn_m_doubles((int)k, (int)c) + (size_t)gemm_nn_grid(std::max<int64_t>(m, 1), (int)c) * pad8((int)c) + 128) * 8;
+  return (gemm_nn_m_doubles((int)k, (int)c) + (size_t)gemm_nn_grid(std::max<int64_t>(m, 1), (int)c) * gemm_nn_part_stride((int)c) + 128) * 8;
 }
 
 int tssvd_matmul(void* stream, int64_t m, int64_t k, int64_t c, const double* X, int64_t ldx,
@@ -783,7 +796,7 @@ int tssvd_matmul(void* stream, int64_t m, int64_t k, int64_t c, const double* X,
     CU(cudaGetLastError());
     CU(launch_gemm_nn(X, ldx, m, (int)k, Mp, (int)c, Y, ldy, nsq ? np : nullptr, s));
     if (nsq)
-      CU(launch_reduce_parts(np, gemm_nn_grid(std::max<int64_t>(m, 1), (int)c), pad8((int)c), c, nsq, s));
+      CU(launch_reduce_parts(np, gemm_nn_grid(std::max<int64_t>(m, 1), (int)c), gemm_nn_part_stride((int)c), c, nsq, s));
     CU(cudaStreamSynchronize(s));
   });
 }

@@ -2,6 +2,7 @@
 // (No code here is shared with oracle/ -- the oracle is plain numpy.)
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace tsk {
@@ -57,6 +58,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+// 2-D tensor TMA load of one box (SASS: UTMALDG); columns c0.., rows r0.. of the
+// tensor map; out-of-bounds elements are zero-filled; completion on `bar`.
+__device__ __forceinline__ void tma_load_2d(void* dst_smem, const CUtensorMap* map, int c0, int r0,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(map), "r"(c0), "r"(r0), "r"(smem_u32(bar))
+      : "memory");
+}
+// named barrier over the consumer warps only (the producer warp never joins)
+__device__ __forceinline__ void bar_consumers(int nthreads) {
+  asm volatile("bar.sync 1, %0;\n" ::"r"(nthreads) : "memory");
+}
+
 // global -> shared bulk copy of `bytes` (multiple of 16, both addresses 16-B aligned)
 __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes,
                                          uint64_t* bar) {

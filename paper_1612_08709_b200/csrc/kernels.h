@@ -24,9 +24,11 @@ cudaError_t launch_reduce_sym(const double* part, int nparts, int w, double* B, 
                               cudaStream_t s);
 
 // Y[:, :c] = X[:, :k] * M  (M row-major, ld = smem_ld(c), rows padded to mult. of 32
-// with zeros).  Optional column sums of squares partials norm_part[g][pad8(c)].
+// with zeros; c <= 256).  Optional column sums of squares partials
+// norm_part[g][gemm_nn_part_stride(c)].
 // In place (Y == X, ldy == ldx) is allowed.
 int gemm_nn_grid(int64_t m, int c);
+int gemm_nn_part_stride(int c);  // doubles per CTA in norm_part (>= pad8(c))
 cudaError_t launch_gemm_nn(const double* X, int64_t ldx, int64_t m, int k, const double* M,
                            int c, double* Y, int64_t ldy, double* norm_part, cudaStream_t s);
 size_t gemm_nn_m_doubles(int k, int c);  // size of the padded M buffer

@@ -145,37 +145,71 @@ __global__ void k_build_k(const double* T, const int* idx2, int r2, const double
 // After the Jacobi SVD of K (column a of `cols`: [P(:, a) (r2) ; J(:, a) (r)]):
 //   V(:, a) = V~_keep J(:, a)  (R = P Sigma (V~_keep J)^T), sign fixed (R5),
 //   sigma[a], V (row-major, ldv), Ps = P * signs (column-major r2 x r2).
-// One warp per output column a < r2.
-__global__ void k_svd_out(const double* cols, int ldc, int r2, int r, const double* vals,
-                          const double* Vt, int w, const int* idx, double* sigma, double* V,
-                          int64_t ldv, double* Ps) {
-  const int a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (a >= r2) return;
-  const double* x = cols + (size_t)a * ldc;
-  // V(:, a) = sum_b Vt(:, idx_b) J(b, a); find the sign from the largest |entry|
-  double best = -1.0, bestv = 0.0;
-  int besti = 1 << 30;
-  for (int i = lane; i < w; i += 32) {
-    double v = 0.0;
-    for (int b = 0; b < r; ++b) v = fma(Vt[(size_t)idx[b] * w + i], x[r2 + b], v);
-    const double av = fabs(v);
-    if (av > best || (av == best && i < besti)) best = av, bestv = v, besti = i;
+// One CTA per 8 output columns; thread i computes row i of V(:, a0:a0+8).
+static constexpr int SVO_COLS = 8;
+__global__ void __launch_bounds__(256) k_svd_out(const double* cols, int ldc, int r2, int r,
+                                                 const double* vals, const double* Vt, int w,
+                                                 const int* idx, double* sigma, double* V, int64_t ldv,
+                                                 double* Ps) {
+  __shared__ double sJ[256][SVO_COLS];
+  __shared__ int sidx[256];
+  __shared__ double sbest[8][SVO_COLS];
+  __shared__ int sbi[8][SVO_COLS];
+  __shared__ double ssign[SVO_COLS];
+  const int a0 = blockIdx.x * SVO_COLS, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int na = min(SVO_COLS, r2 - a0);
+  for (int e = tid; e < r * SVO_COLS; e += blockDim.x) {
+    const int bb = e / SVO_COLS, q = e % SVO_COLS;
+    sJ[bb][q] = q < na ? cols[(size_t)(a0 + q) * ldc + r2 + bb] : 0.0;
   }
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-    const double ov = __shfl_xor_sync(0xffffffffu, bestv, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, besti, o);
-    if (ob > best || (ob == best && oi < besti)) best = ob, bestv = ov, besti = oi;
+  for (int bb = tid; bb < r; bb += blockDim.x) sidx[bb] = idx[bb];
+  __syncthreads();
+  double v[SVO_COLS];
+#pragma unroll
+  for (int q = 0; q < SVO_COLS; ++q) v[q] = 0.0;
+  const int i = tid;
+  if (i < w)
+    for (int bb = 0; bb < r; ++bb) {
+      const double x = Vt[(size_t)sidx[bb] * w + i];
+#pragma unroll
+      for (int q = 0; q < SVO_COLS; ++q) v[q] = fma(x, sJ[bb][q], v[q]);
+    }
+  // sign of each column: its largest-|.| entry positive (ties -> lowest index)
+#pragma unroll
+  for (int q = 0; q < SVO_COLS; ++q) {
+    double bv = i < w ? fabs(v[q]) : -1.0;
+    int bi = i < w ? i : (1 << 30);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) bv = ov, bi = oi;
+    }
+    if (lane == 0) sbest[warp][q] = bv, sbi[warp][q] = bi;
   }
-  const double sg = bestv < 0.0 ? -1.0 : 1.0;
-  for (int i = lane; i < w; i += 32) {
-    double v = 0.0;
-    for (int b = 0; b < r; ++b) v = fma(Vt[(size_t)idx[b] * w + i], x[r2 + b], v);
-    V[(size_t)i * ldv + a] = sg * v;
+  __syncthreads();
+  if (tid < SVO_COLS) {
+    double bv = -1.0;
+    int bi = 1 << 30;
+    for (int ww = 0; ww < (int)(blockDim.x >> 5); ++ww)
+      if (sbest[ww][tid] > bv || (sbest[ww][tid] == bv && sbi[ww][tid] < bi)) bv = sbest[ww][tid], bi = sbi[ww][tid];
+    ssign[tid] = 1.0;  // resolved below by the owner of row bi
+    sbi[0][tid] = bi;
   }
-  for (int c = lane; c < r2; c += 32) Ps[(size_t)a * r2 + c] = sg * x[c];
-  if (lane == 0) sigma[a] = vals[a];
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < SVO_COLS; ++q)
+    if (i == sbi[0][q] && i < w) ssign[q] = v[q] < 0.0 ? -1.0 : 1.0;
+  __syncthreads();
+  if (i < w)
+#pragma unroll
+    for (int q = 0; q < SVO_COLS; ++q)
+      if (q < na) V[(size_t)i * ldv + a0 + q] = ssign[q] * v[q];
+  for (int e = tid; e < na * r2; e += blockDim.x) {
+    const int q = e / r2, c = e % r2;
+    Ps[(size_t)(a0 + q) * r2 + c] = ssign[q] * cols[(size_t)(a0 + q) * ldc + c];
+  }
+  if (tid < na) sigma[a0 + tid] = vals[a0 + tid];
 }
 
 // M2 (nc x r2 row-major padded): M2[idx_b][a] = sum_c W(b, idx2_c) / (sig[idx_b] T[idx2_c]) Ps(c, a)
@@ -260,8 +294,7 @@ void build_k(const double* T, const int* idx2, int r2, const double* W, int r, c
 void svd_out(const double* cols, int ldc, int r2, int r, const double* vals, const double* Vt,
              int w, const int* idx, double* sigma, double* V, int64_t ldv, double* Ps,
              cudaStream_t s) {
-  k_svd_out<<<nb((int64_t)r2 * 32, 256), 256, 0, s>>>(cols, ldc, r2, r, vals, Vt, w, idx, sigma, V,
-                                                     ldv, Ps);
+  k_svd_out<<<nb(r2, SVO_COLS), 256, 0, s>>>(cols, ldc, r2, r, vals, Vt, w, idx, sigma, V, ldv, Ps);
 }
 void build_m2(const double* W, int r, const int* idx, const double* sig, const double* T,
               const int* idx2, int r2, const double* Ps, double* M2, int ldm, cudaStream_t s) {
