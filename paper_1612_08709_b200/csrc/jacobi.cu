@@ -111,7 +111,7 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
   return y;
 }
 
-template <int C, int G, int V, bool REG>
+template <int C, int G, int V>
 __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
   Cl<C> cl;
   const int h = cl.rank();
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
   double* X = dsm;                                 // [nslots][P]
   double* bc = X + (size_t)(nslots + 1) * P;       // [JMAX] pivot row (EIG, C > 1)
   double* xch = bc + JMAX;                         // C > 1: [2][JMAXP][C][4] pair partials
-  double* nx = xch + (REG ? 4 * JW * V * G : (C > 1 ? 2 * JMAXP * C * 4 : 0));  // [C][JMAX] norms
+  double* nx = xch + (C > 1 ? 2 * JMAXP * C * 4 : 0);  // [C][JMAX] partial column norms
 
   // ------------------------------------------------------------ load ----
   for (int r = tid; r < P; r += JT) X[(size_t)nslots * P + r] = 0.0;  // the zero (pad) slot
@@ -314,126 +314,7 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
   const long long t_chol = clock64();
   int sweep = 0, rounds = 0;
   bool converged = K <= 1;
-  if constexpr (REG) {
-    // Register-resident sweeps (one CTA).  Group i (G lanes) holds the pair
-    // (T_i, B_i) of the circle ordering in registers, lane gl rows gl + G e.
-    // After each round the columns move one group along the ring
-    //   T_i <- T_{i+1} (T_{m-1} <- B_{m-1}),  B_i <- B_{i-1} (B_0 <- T_1),  T_0 fixed,
-    // by shuffles inside a warp and through shared memory across warps, so a
-    // round moves 2 columns per pair instead of loading and storing 4.  After
-    // a full sweep (NE-1 rounds) every column is back where it started.
-    const int NE = K + (K & 1), m = NE / 2;
-    if (K & 1) s_order[K] = nslots;  // the zero pad column
-    __syncthreads();
-    constexpr int GPW = 32 / G;
-    const int grp = lane / G, gl = lane % G;
-    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
-    const int gi = warp * GPW + grp;  // group index
-    const bool act = gi < m;
-    const int nwarps_act = (m + GPW - 1) / GPW;
-    const int dloc = max(0, min(nloc, a.dpad - row0));
-    double T[V], B[V];
-    const int sT = act ? s_order[gi] : nslots, sB = act ? s_order[NE - 1 - gi] : nslots;
-#pragma unroll
-    for (int e = 0; e < V; ++e) {
-      const int r = gl + G * e;
-      T[e] = r < nloc ? X[sT * P + r] : 0.0;
-      B[e] = r < nloc ? X[sB * P + r] : 0.0;
-    }
-    // cross-warp exchange buffers [parity][warp][V][G]: xT from slot 0, xB from the last slot
-    double* xT = xch;
-    double* xB = xch + 2 * JW * V * G;
-    __syncthreads();
-    for (; sweep < a.max_sweeps && !converged; ++sweep) {
-      int any = 0;
-      for (int r = 0; r < NE - 1; ++r, ++rounds) {
-        int rot = 0;
-        if (act) {
-          double al = 0.0, be = 0.0, ga = 0.0, al1 = 0.0, be1 = 0.0, ga1 = 0.0;
-#pragma unroll
-          for (int e = 0; e < V; e += 2) {
-            if (gl + G * e < dloc) {
-              al = fma(T[e], T[e], al);
-              be = fma(B[e], B[e], be);
-              ga = fma(T[e], B[e], ga);
-            }
-            if (e + 1 < V && gl + G * (e + 1) < dloc) {
-              al1 = fma(T[e + 1], T[e + 1], al1);
-              be1 = fma(B[e + 1], B[e + 1], be1);
-              ga1 = fma(T[e + 1], B[e + 1], ga1);
-            }
-          }
-          al += al1;
-          be += be1;
-          ga += ga1;
-#pragma unroll
-          for (int o = G / 2; o > 0; o >>= 1) {
-            al += __shfl_xor_sync(gmask, al, o);
-            be += __shfl_xor_sync(gmask, be, o);
-            ga += __shfl_xor_sync(gmask, ga, o);
-          }
-          if (ga != 0.0 && ga * ga > tol2 * al * be && fmax(al, be) > skip2) {
-            double d = be - al, g2 = ga + ga;
-            const double big = fmax(fabs(d), fabs(g2));
-            const int ex = (int)((__double_as_longlong(big) >> 52) & 0x7ff);
-            const double sc = __longlong_as_double((long long)(2046 - ex) << 52);
-            d *= sc;
-            g2 *= sc;
-            const double w = fma(d, d, g2 * g2);
-            const double root = w * rsqrt_nr(w);
-            const double t = (d >= 0.0 ? g2 : -g2) * rcp_nr(fabs(d) + root);
-            const double c = rsqrt_nr(fma(t, t, 1.0));
-            const double sn = c * t;
-#pragma unroll
-            for (int e = 0; e < V; ++e) {
-              const double u = T[e], v = B[e];
-              T[e] = fma(c, u, -sn * v);
-              B[e] = fma(sn, u, c * v);
-            }
-            rot = 1;
-          }
-        }
-        // boundary columns leave through shared memory
-        const int par = rounds & 1;
-        if (warp < nwarps_act) {
-          if (grp == 0)
-#pragma unroll
-            for (int e = 0; e < V; ++e) xT[((par * JW + warp) * V + e) * G + gl] = T[e];
-          if (grp == GPW - 1)
-#pragma unroll
-            for (int e = 0; e < V; ++e) xB[((par * JW + warp) * V + e) * G + gl] = B[e];
-        }
-        any |= __syncthreads_or(rot);
-        // move: T_i <- T_{i+1}, B_i <- B_{i-1}; ends of the ring special
-#pragma unroll
-        for (int e = 0; e < V; ++e) {
-          double tn = __shfl_down_sync(0xffffffffu, T[e], G);  // T of group gi+1 (same warp)
-          double bn = __shfl_up_sync(0xffffffffu, B[e], G);    // B of group gi-1 (same warp)
-          if (grp == GPW - 1 && warp + 1 < nwarps_act) tn = xT[((par * JW + warp + 1) * V + e) * G + gl];
-          if (grp == 0 && warp > 0) bn = xB[((par * JW + warp - 1) * V + e) * G + gl];
-          if (gi == m - 1) tn = B[e];  // T_{m-1} <- B_{m-1}
-          if (gi == 0) {               // T_0 fixed, B_0 <- T_1
-            bn = tn;
-            tn = T[e];
-          }
-          T[e] = tn;
-          B[e] = bn;
-        }
-      }
-      converged = !any;
-    }
-    // every column is back at its starting group: write the pairs back to their slots
-    if (act)
-#pragma unroll
-      for (int e = 0; e < V; ++e) {
-        const int r = gl + G * e;
-        if (r < nloc) {
-          X[sT * P + r] = T[e];
-          X[sB * P + r] = B[e];
-        }
-      }
-    __syncthreads();
-  } else {
+  {
   // Circle (round-robin) ordering on positions 0..NE-1: in round r, pair i is
   // (p, q) = (i ? 1 + (i-1+r) mod (NE-1) : 0, 1 + (NE-2-i+r) mod (NE-1)),
   // advanced incrementally.  An odd K is padded with the all-zero slot
@@ -573,9 +454,9 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
 }
 
 // ------------------------------------------------------------- launch ----
-template <int C, int G, int V, bool REG>
+template <int C, int G, int V>
 static cudaError_t jac_go(const JacArgs& a, size_t smem, cudaStream_t s) {
-  auto kern = jacobi_kernel<C, G, V, REG>;
+  auto kern = jacobi_kernel<C, G, V>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -596,38 +477,18 @@ static cudaError_t jac_go(const JacArgs& a, size_t smem, cudaStream_t s) {
 template <int C, int G>
 static cudaError_t jac_v(const JacArgs& a, size_t smem, cudaStream_t s) {
   switch (a.V) {
-    case 2: return jac_go<C, G, 2, false>(a, smem, s);
-    case 4: return jac_go<C, G, 4, false>(a, smem, s);
-    case 6: return jac_go<C, G, 6, false>(a, smem, s);
-    default: return jac_go<C, G, 8, false>(a, smem, s);
-  }
-}
-
-template <int G>
-static cudaError_t jac_reg_v(const JacArgs& a, size_t smem, cudaStream_t s) {
-  switch (a.V) {
-    case 2: return jac_go<1, G, 2, true>(a, smem, s);
-    case 4: return jac_go<1, G, 4, true>(a, smem, s);
-    case 6: return jac_go<1, G, 6, true>(a, smem, s);
-    case 8: return jac_go<1, G, 8, true>(a, smem, s);
-    case 10: return jac_go<1, G, 10, true>(a, smem, s);
-    case 12: return jac_go<1, G, 12, true>(a, smem, s);
-    case 14: return jac_go<1, G, 14, true>(a, smem, s);
-    default: return jac_go<1, G, 16, true>(a, smem, s);
+    case 2: return jac_go<C, G, 2>(a, smem, s);
+    case 3: return jac_go<C, G, 3>(a, smem, s);
+    case 4: return jac_go<C, G, 4>(a, smem, s);
+    case 5: return jac_go<C, G, 5>(a, smem, s);
+    case 6: return jac_go<C, G, 6>(a, smem, s);
+    case 7: return jac_go<C, G, 7>(a, smem, s);
+    default: return jac_go<C, G, 8>(a, smem, s);
   }
 }
 
 template <int C>
-static cudaError_t jac_g(const JacArgs& a, int g, bool reg, size_t smem, cudaStream_t s) {
-  if constexpr (C == 1) {
-    if (reg) {
-      switch (g) {
-        case 4: return jac_reg_v<4>(a, smem, s);
-        case 8: return jac_reg_v<8>(a, smem, s);
-        default: return jac_reg_v<16>(a, smem, s);
-      }
-    }
-  }
+static cudaError_t jac_g(const JacArgs& a, int g, size_t smem, cudaStream_t s) {
   switch (g) {
     case 4: return jac_v<C, 4>(a, smem, s);
     case 8: return jac_v<C, 8>(a, smem, s);
@@ -636,34 +497,25 @@ static cudaError_t jac_g(const JacArgs& a, int g, bool reg, size_t smem, cudaStr
 }
 
 // dynamic shared memory (doubles): slots (+ zero slot), pivot row, exchange, norms
-static size_t jac_smem(int C, int nslots, int P, size_t xch) {
-  return ((size_t)(nslots + 1) * P + JMAX + xch + (size_t)C * JMAX) * 8;
+static size_t jac_smem(int C, int nslots, int P) {
+  return ((size_t)(nslots + 1) * P + JMAX + (C > 1 ? 2 * JMAXP * C * 4 : 0) + (size_t)C * JMAX) * 8;
 }
 
-// Round cost models (cycles; B200 measured: DFMA/DADD 7-cycle latency, 2 issue
+// Round cost model (cycles; B200 measured: DFMA/DADD 7-cycle latency, 2 issue
 // cycles per warp-instruction on the 16-lane FP64 unit, SHFL+DADD 35, LDS 29,
-// SHFL/LDS bandwidth 128 B/cycle/SM, MUFU f64 ~19, the rotation parameters
-// ~230 on the critical path; a cluster round (DSMEM exchange + barrier with
-// its membar) ~2500).
-static double jac_cost_smem(int C, int G, int V, int npairs) {
+// shared-memory bandwidth 128 B/cycle/SM, MUFU f64 ~19; the rotation
+// parameters ~230 on the critical path; a cluster round (DSMEM exchange +
+// barrier with its membar) ~2500).  A round reads and writes both columns of
+// every pair, so one CTA is shared-memory-bandwidth bound.
+static double jac_round_cost(int C, int G, int V, int npairs) {
   const int warps = (int)ceil_div(npairs, 32 / G);
   const int per_smsp = (int)ceil_div(warps, 4);
   int lg = 0;
   while ((1 << lg) < G) ++lg;
   const double pipe = 2.0 * per_smsp * (14.0 * V + 3.0 * lg + 35.0);
-  const double smem = 2.0 * npairs * (2.0 * G * V) * 16.0 / 128.0;  // read + write both columns
+  const double smem = 2.0 * npairs * (2.0 * G * V) * 16.0 / 128.0 / C;
   const double chain = 60.0 + 9.0 * V + 35.0 * lg + 230.0 + 16.0 * V;
   return std::max(pipe, smem) + chain + (C > 1 ? 2500.0 : 50.0);
-}
-static double jac_cost_reg(int G, int V, int npairs) {
-  const int warps = (int)ceil_div(npairs, 32 / G);
-  const int per_smsp = (int)ceil_div(warps, 4);
-  int lg = 0;
-  while ((1 << lg) < G) ++lg;
-  const double pipe = 2.0 * per_smsp * (7.0 * V + 3.0 * lg + 45.0);
-  const double shfl = warps * 4.0 * V;
-  const double chain = 3.5 * V + 35.0 * lg + 230.0 + 110.0;
-  return std::max(pipe, shfl) + chain;
 }
 
 static cudaError_t jac_dispatch(JacArgs a, cudaStream_t s) {
@@ -672,48 +524,32 @@ static cudaError_t jac_dispatch(JacArgs a, cudaStream_t s) {
   if (nslots > JMAX || a.L > 2 * JMAX) return cudaErrorInvalidValue;
   const size_t budget = dev_info().smem_optin - 8 * 1024;  // static shared + slack
   const int npairs = (nslots + 1) / 2;
-  // tuning overrides (experiments only): TSSVD_JAC_G, TSSVD_JAC_C, TSSVD_JAC_REG
+  // tuning overrides (experiments only): TSSVD_JAC_G, TSSVD_JAC_C
   static const int force_g = getenv("TSSVD_JAC_G") ? atoi(getenv("TSSVD_JAC_G")) : 0;
   static const int force_c = getenv("TSSVD_JAC_C") ? atoi(getenv("TSSVD_JAC_C")) : 0;
-  // register-resident sweeps measured slower than the shared-memory ones on B200 (issue-bound
-  // move/select overhead): opt-in only, kept for tuning
-  static const int force_r = getenv("TSSVD_JAC_REG") ? atoi(getenv("TSSVD_JAC_REG")) : 0;
   double best = 1e300;
-  int bC = 0, bG = 0, bV = 0, bLh = 0, bP = 0;
-  bool bR = false;
-  size_t bsm = 0;
+  int bC = 0, bG = 0, bV = 0, bLh = 0;
   for (int C = 1; C <= 4; C *= 2) {
     const int Lh = (int)((ceil_div(a.L, C) + 1) & ~1);
     for (int G = 4; G <= 16; G *= 2) {
       if (JW * (32 / G) < npairs) continue;  // one pass over the pairs
       if ((force_g && G != force_g) || (force_c && C != force_c)) continue;
-      // register-resident sweeps (one CTA)
-      if (C == 1 && force_r == 1) {
-        int V = (int)ceil_div(Lh, G);
-        V = V <= 2 ? 2 : (V + 1) & ~1;
-        const size_t sm = jac_smem(1, nslots, Lh, (size_t)4 * JW * V * G);
-        if (V <= 16 && sm <= budget) {
-          const double cost = jac_cost_reg(G, V, npairs);
-          if (cost < best) best = cost, bC = 1, bG = G, bV = V, bLh = Lh, bP = Lh, bR = true, bsm = sm;
-        }
-      }
-      if (force_r == 1) continue;
       int V = (int)ceil_div(Lh, 2 * G);
       if (V > 8) continue;
-      V = V <= 2 ? 2 : (V + 1) & ~1;  // instantiated: 2, 4, 6, 8
-      const size_t sm = jac_smem(C, nslots, 2 * G * V, C > 1 ? (size_t)2 * JMAXP * C * 4 : 0);
-      if (sm > budget) continue;
-      const double cost = jac_cost_smem(C, G, V, npairs);
-      if (cost < best) best = cost, bC = C, bG = G, bV = V, bLh = Lh, bP = 2 * G * V, bR = false, bsm = sm;
+      V = std::max(V, 2);
+      if (jac_smem(C, nslots, 2 * G * V) > budget) continue;
+      const double cost = jac_round_cost(C, G, V, npairs);
+      if (cost < best) best = cost, bC = C, bG = G, bV = V, bLh = Lh;
     }
   }
   if (!bC) return cudaErrorInvalidValue;
   a.Lh = bLh;
   a.V = bV;
-  a.P = bP;
-  if (bC == 1) return jac_g<1>(a, bG, bR, bsm, s);
-  if (bC == 2) return jac_g<2>(a, bG, false, bsm, s);
-  return jac_g<4>(a, bG, false, bsm, s);
+  a.P = 2 * bG * bV;
+  const size_t smem = jac_smem(bC, nslots, a.P);
+  if (bC == 1) return jac_g<1>(a, bG, smem, s);
+  if (bC == 2) return jac_g<2>(a, bG, smem, s);
+  return jac_g<4>(a, bG, smem, s);
 }
 
 cudaError_t launch_jacobi_eig(const double* B, int ldb, int n, double tol, double trunc,
