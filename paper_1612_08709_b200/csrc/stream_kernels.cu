@@ -100,22 +100,25 @@ __device__ __forceinline__ void ring_init(Ring r, int nst, int consumers) {
 
 // ============================================================== SYRK (Gram) ==
 // CTA b owns rows [b*rpc, (b+1)*rpc) (rpc a multiple of KR, so only the last
-// CTA's last box can cross m -- and there TMA zero-fills).  Output tiles of B
-// are 8x8 DMMA tiles in the lower triangle, grouped in 2x2 "units" (16x16) so
-// each fragment load feeds two MMAs.  Both operands are columns of the same
+// CTA's last box can cross m -- and there TMA zero-fills).  The T = nb(nb+1)/2
+// lower-triangle 8x8 DMMA tiles of B, in row-major order (0,0), (1,0), (1,1),
+// (2,0), ..., are dealt to the consumer warps in contiguous, equal runs of at
+// most SYRK_TPW tiles (grid.y splits the list when one CTA cannot hold it), so
+// every warp issues the same number of DMMAs per stage and consecutive tiles
+// of a run share their row fragment.  Both operands are columns of the same
 // row block: the fragment of column block c at k-step kk is Xs[kk*4+t][c*8+g]
 // in the A (= X^T) and the B role alike.
 static constexpr int SYRK_KR = 32;
+static constexpr int SYRK_TPW = 8;
 
-template <int UPW>
-__global__ void __launch_bounds__(512) syrk_kernel(const __grid_constant__ CUtensorMap tx, int64_t m,
-                                                   int w, int W, int64_t rpc, double* __restrict__ part,
-                                                   int nst, int ups) {
+__global__ void __launch_bounds__(512, 2) syrk_kernel(const __grid_constant__ CUtensorMap tx, int64_t m,
+                                                      int w, int W, int64_t rpc, double* __restrict__ part,
+                                                      int nst, int tps, int tpw) {
   extern __shared__ __align__(128) unsigned char smem[];
   const Ring ring{reinterpret_cast<uint64_t*>(smem)};
   double* buf = reinterpret_cast<double*>(smem + kBarBytes);
   const int stage_d = SYRK_KR * W;
-  const int nb = (w + 7) >> 3, nu = (nb + 1) >> 1, nunits = nu * (nu + 1) / 2;
+  const int nb = (w + 7) >> 3, ntiles = nb * (nb + 1) / 2;
   const int wp = nb * 8;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int ncw = (blockDim.x >> 5) - 1;  // consumer warps (warp 0 produces)
@@ -134,49 +137,33 @@ __global__ void __launch_bounds__(512) syrk_kernel(const __grid_constant__ CUten
       }
     return;
   }
-  const int cw = warp - 1;
-  // this warp's units (ui >= uj), decoded from the linear lower-triangle index
-  int ci0[UPW], ci1[UPW], cj0[UPW], cj1[UPW];
-  bool uv[UPW], dg[UPW], vi1[UPW], vj1[UPW];
-  const int ubase = blockIdx.y * ups, uend = min(nunits, ubase + ups);
+  // this warp's run of tiles [q0, q1) of the row-major lower triangle
+  const int q0 = min(ntiles, blockIdx.y * tps + (warp - 1) * tpw);
+  const int q1 = min(ntiles, min(blockIdx.y * tps + tps, q0 + tpw));
+  const int nt = q1 - q0;
+  int I0 = 0;
+  while ((I0 + 1) * (I0 + 2) / 2 <= q0) ++I0;
+  const int J0 = q0 - I0 * (I0 + 1) / 2;
+  double acc[SYRK_TPW][2];
 #pragma unroll
-  for (int k = 0; k < UPW; ++k) {
-    const int u = ubase + cw + k * ncw;
-    uv[k] = u < uend;
-    int ui = 0;
-    while ((ui + 1) * (ui + 2) / 2 <= u) ++ui;
-    const int uj = u - ui * (ui + 1) / 2;
-    dg[k] = ui == uj;
-    vi1[k] = 2 * ui + 1 < nb;
-    vj1[k] = 2 * uj + 1 < nb;
-    ci0[k] = (2 * ui) * 8 + g;
-    ci1[k] = vi1[k] ? (2 * ui + 1) * 8 + g : g;
-    cj0[k] = (2 * uj) * 8 + g;
-    cj1[k] = vj1[k] ? (2 * uj + 1) * 8 + g : g;
-    if (!uv[k]) ci0[k] = ci1[k] = cj0[k] = cj1[k] = g;
-  }
-  double acc[UPW][4][2];
-#pragma unroll
-  for (int k = 0; k < UPW; ++k)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[k][q][0] = acc[k][q][1] = 0.0;
+  for (int k = 0; k < SYRK_TPW; ++k) acc[k][0] = acc[k][1] = 0.0;
 
   for (int s = 0; s < nsteps; ++s) {
     const int b = s % nst;
     mbar_wait(ring.full(b), (s / nst) & 1);
-    const double* base = buf + b * stage_d + t * W;
+    const double* base = buf + b * stage_d + t * W + g;
 #pragma unroll
-    for (int kk = 0; kk < SYRK_KR / 4; ++kk) {
+    for (int kk = 0; kk < SYRK_KR / 4 && nt > 0; ++kk) {
       const double* rp = base + kk * 4 * W;
+      double fi = rp[I0 * 8];
+      int I = I0, J = J0;
 #pragma unroll
-      for (int k = 0; k < UPW; ++k) {
-        if (!uv[k]) continue;
-        const double fi0 = rp[ci0[k]], fi1 = rp[ci1[k]];
-        const double fj0 = rp[cj0[k]], fj1 = rp[cj1[k]];
-        dmma(acc[k][0], fi0, fj0);
-        if (!dg[k] && vj1[k]) dmma(acc[k][1], fi0, fj1);
-        if (vi1[k]) dmma(acc[k][2], fi1, fj0);
-        if (vi1[k] && vj1[k]) dmma(acc[k][3], fi1, fj1);
+      for (int k = 0; k < SYRK_TPW; ++k) {
+        if (k < nt) {
+          if (k > 0 && J == 0) fi = rp[I * 8];  // a new block row starts
+          dmma(acc[k], fi, rp[J * 8]);
+        }
+        if (++J > I) ++I, J = 0;
       }
     }
     __syncwarp();
@@ -184,49 +171,47 @@ __global__ void __launch_bounds__(512) syrk_kernel(const __grid_constant__ CUten
   }
 
   double* P = part + (size_t)blockIdx.x * wp * wp;
+  int I = I0, J = J0;
 #pragma unroll
-  for (int k = 0; k < UPW; ++k) {
-    if (!uv[k]) continue;
-    const int u = ubase + cw + k * ncw;
-    int ui = 0;
-    while ((ui + 1) * (ui + 2) / 2 <= u) ++ui;
-    const int uj = u - ui * (ui + 1) / 2;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int I = 2 * ui + (q >> 1), J = 2 * uj + (q & 1);
-      if (I >= nb || J >= nb || J > I) continue;
+  for (int k = 0; k < SYRK_TPW; ++k) {
+    if (k < nt)
       *reinterpret_cast<double2*>(P + (size_t)(I * 8 + g) * wp + J * 8 + 2 * t) =
-          make_double2(acc[k][q][0], acc[k][q][1]);
-    }
+          make_double2(acc[k][0], acc[k][1]);
+    if (++J > I) ++I, J = 0;
   }
 }
 
-// Units per consumer warp (UPW), consumer warps and unit splits (grid.y): at
-// most 15 consumer warps and 4 units (32 accumulator doubles) per warp; beyond
-// 60 units the units are split over grid.y CTAs that read the same rows.
-static int syrk_upw(int w, int* ncw_out, int* splits_out = nullptr, int* ups_out = nullptr) {
-  const int nb = (w + 7) / 8, nu = (nb + 1) / 2, nunits = nu * (nu + 1) / 2;
-  const int splits = (int)ceil_div(nunits, 60);
-  const int ups = (int)ceil_div(nunits, splits);
-  const int upw = (int)ceil_div(ups, 15);
-  *ncw_out = (int)ceil_div(ups, upw);
-  if (splits_out) *splits_out = splits;
-  if (ups_out) *ups_out = ups;
-  return upw;
+// Tiles per warp, consumer warps and tile-list splits over grid.y: equal runs,
+// <= 15 consumers, <= SYRK_TPW tiles each; among equal split counts the warp
+// count with the least padding wins.
+struct SyrkPlan {
+  int splits, tps, tpw, ncw;
+};
+static SyrkPlan syrk_plan(int w) {
+  const int nb = (w + 7) / 8, ntiles = nb * (nb + 1) / 2;
+  SyrkPlan p{};
+  p.splits = (int)ceil_div(ntiles, 15 * SYRK_TPW);
+  p.tps = (int)ceil_div(ntiles, p.splits);
+  // long runs amortise the row fragment and the stage hand-off; short runs only
+  // when a long one would leave a warp idle
+  double best = 1e300;
+  for (int tpw = SYRK_TPW; tpw >= 1; --tpw) {
+    const int ncw = (int)ceil_div(p.tps, tpw);
+    if (ncw > 15) break;
+    const double score = (double)(tpw * ncw - p.tps) / p.tps + (tpw < 6 && p.tps >= 6 * ncw ? 0.2 : 0.0) +
+                         (tpw < 6 ? 0.05 * (6 - tpw) : 0.0);
+    if (score < best - 1e-12) best = score, p.ncw = ncw, p.tpw = tpw;
+  }
+  return p;
 }
 
 static size_t syrk_stage_bytes(int w) { return (size_t)SYRK_KR * std::min(smem_ld(w), 256) * 8; }
 
-static int syrk_nst(int w) {
-  const size_t budget = dev_info().smem_optin - kBarBytes;
-  return (int)std::max<size_t>(2, std::min<size_t>(8, budget / syrk_stage_bytes(w)));
-}
-
+// CTAs per SM: by shared memory (>= 4 stages each) and threads, at most 4
 int syrk_partials_grid(int64_t m, int w) {
-  int ncw;
-  syrk_upw(w, &ncw);
-  const size_t smem = kBarBytes + (size_t)std::min(syrk_nst(w), 4) * syrk_stage_bytes(w);
-  int per_sm = (int)std::max<size_t>(1, std::min<size_t>(228 * 1024 / (smem + 1024), 2048 / (32 * (ncw + 1))));
+  const SyrkPlan p = syrk_plan(w);
+  const size_t smem = kBarBytes + (size_t)4 * syrk_stage_bytes(w);
+  int per_sm = (int)std::max<size_t>(1, std::min<size_t>(228 * 1024 / (smem + 1024), 2048 / (32 * (p.ncw + 1))));
   per_sm = std::min(per_sm, 4);
   int64_t g = (int64_t)dev_info().sms * per_sm;
   int64_t maxg = std::max<int64_t>(1, ceil_div(m, SYRK_KR));
@@ -238,20 +223,9 @@ size_t syrk_partials_doubles(int64_t m, int w) {
   return (size_t)syrk_partials_grid(m, w) * wp * wp;
 }
 
-template <int UPW>
-static cudaError_t syrk_go(dim3 grid, int ncw, size_t smem, const CUtensorMap& tx, int64_t m, int w,
-                           int W, int64_t rpc, double* part, int nst, int ups, cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute(syrk_kernel<UPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
-  if (e != cudaSuccess) return e;
-  syrk_kernel<UPW><<<grid, (ncw + 1) * 32, smem, s>>>(tx, m, w, W, rpc, part, nst, ups);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_syrk(const double* X, int64_t ldx, int64_t m, int w, double* part,
                         cudaStream_t s) {
-  int ncw, splits, ups;
-  const int upw = syrk_upw(w, &ncw, &splits, &ups);
+  const SyrkPlan p = syrk_plan(w);
   const int gx = syrk_partials_grid(m, w);
   const int W = std::min(smem_ld(w), 256);  // TMA box limit (w > 248: conflicted but correct)
   const int per_sm = std::max(1, (int)ceil_div(gx, dev_info().sms));
@@ -266,13 +240,10 @@ cudaError_t launch_syrk(const double* X, int64_t ldx, int64_t m, int w, double* 
   CUtensorMap tx;
   cudaError_t e = make_tmap(&tx, X, m, w, ldx, SYRK_KR, W);
   if (e != cudaSuccess) return e;
-  const dim3 grid(gx, splits);
-  switch (upw) {
-    case 1: return syrk_go<1>(grid, ncw, smem, tx, m, w, W, rpc, part, nst, ups, s);
-    case 2: return syrk_go<2>(grid, ncw, smem, tx, m, w, W, rpc, part, nst, ups, s);
-    case 3: return syrk_go<3>(grid, ncw, smem, tx, m, w, W, rpc, part, nst, ups, s);
-    default: return syrk_go<4>(grid, ncw, smem, tx, m, w, W, rpc, part, nst, ups, s);
-  }
+  e = cudaFuncSetAttribute(syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  syrk_kernel<<<dim3(gx, p.splits), (p.ncw + 1) * 32, smem, s>>>(tx, m, w, W, rpc, part, nst, p.tps, p.tpw);
+  return cudaGetLastError();
 }
 
 // Fixed-order sum over partials by one warp per output element: lane l sums
