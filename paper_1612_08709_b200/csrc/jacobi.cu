@@ -172,6 +172,102 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
     const double tabs = a.trunc * gmax;
     cl.sync();
 
+    bool done = false;
+    if constexpr (C == 1) {
+      if (n <= 128) {
+        // ---- diagonally pivoted Cholesky with the Schur complement in registers ----
+        // Thread (warp w, lane l) owns S[r][c] for rows r = l + 32 i (i < 4) and
+        // slots c = w + 16 j (j < 8).  Step k with pivot p: the owner warp of
+        // slot p publishes column p (pcol) and writes X[:, k] = pcol / sqrt(S_pp)
+        // (zero on rows pivoted earlier) into slot k; every thread updates its
+        // elements S[r][c] -= pcol[r] pcol[c] / S_pp; the owners of diagonal
+        // elements publish them for the next argmax.  Two barriers per step.
+        double* diag = bc;  // [n]
+        double* pcol = nx;  // [n]
+        double Sr[8][4];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int c = warp + JW * j, r = lane + 32 * i;
+            Sr[j][i] = (c < n && r < n) ? X[c * P + r] : 0.0;
+          }
+        // diagonal element r (r = lane + 32 i) lives in slot j = r / 16 of warp r % 16
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int r = lane + 32 * i;
+            if (r < n && warp + JW * j == r) diag[r] = Sr[j][i];
+          }
+        __syncthreads();  // S is in registers: the slots are free for X
+        uint32_t rmask = 0, smask = 0;  // pivoted rows (bit i) / slots (bit j) of this thread
+        int k = 0;
+        for (; k < n; ++k) {
+          double bv = -1.0;
+          int bi = -1;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int r = lane + 32 * i;
+            if (r < n && !((rmask >> i) & 1)) {
+              double d = diag[r];
+              if (isnan(d)) d = INFINITY;  // non-finite input: pivot it (NaN spreads, caught downstream)
+              if (bi < 0 || d > bv) bv = d, bi = r;
+            }
+          }
+          warp_argmax(bv, bi);
+          const int p = bi;
+          const double dp = bv;
+          if (p < 0 || !(dp > tabs)) break;  // uniform over the CTA
+          const double rsq = 1.0 / sqrt(dp);
+          if ((p % JW) == warp) {  // owner of slot p: publish column p, write X[:, k]
+            const int jp = p / JW;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int r = lane + 32 * i;
+              double v = 0.0;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) v = j == jp ? Sr[j][i] : v;
+              if (r < n) {
+                pcol[r] = v;
+                X[k * P + r] = ((rmask >> i) & 1) ? 0.0 : v * rsq;
+              }
+            }
+          }
+          if (tid == 0) s_order[k] = k;
+          __syncthreads();
+          const double inv = 1.0 / dp;
+          double pr[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int r = lane + 32 * i;
+            pr[i] = (r < n && r != p && !((rmask >> i) & 1)) ? pcol[r] * inv : 0.0;
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int c = warp + JW * j;
+            if (c < n && c != p && !((smask >> j) & 1)) {
+              const double f = pcol[c];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) Sr[j][i] = fma(-pr[i], f, Sr[j][i]);
+            }
+          }
+          if (((p - lane) & 31) == 0) rmask |= 1u << (p >> 5);
+          if ((p % JW) == warp) smask |= 1u << (p / JW);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int r = lane + 32 * i;
+              if (r < n && warp + JW * j == r && !((rmask >> i) & 1)) diag[r] = Sr[j][i];
+            }
+          __syncthreads();
+        }
+        K = k;
+        done = true;
+      }
+    }
+    if (!done) {
     // ---- diagonally pivoted Cholesky, right-looking, in place ----
     // Step k with pivot p: X[:, k] := S[:, p] / sqrt(S_pp), stored in slot p
     // (zero on rows pivoted earlier; finalised one step late, when slot p is no
@@ -276,6 +372,7 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
         const bool dead = s_rank[gr] != 0 && gr != prev;
         xs[e] = dead ? 0.0 : xs[e] * rsq;
       }
+    }
     }
   } else {
     for (int i = tid; i < nslots; i += JT) s_order[i] = i;
