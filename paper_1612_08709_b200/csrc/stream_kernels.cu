@@ -347,9 +347,14 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
   for (int i = 0; i < MI; ++i)
 #pragma unroll
     for (int j = 0; j < NIW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  // per-warp column sums of squares (norm epilogue), in shared memory after the stages
+  // per-warp column sums of squares (norm epilogue): in registers over the whole
+  // run when they fit (NRM), else per tile into a shared-memory row after the stages
+  constexpr bool NRM = 2 * MI * NIW + 2 * NIW <= 48;
+  double nacc[NRM ? NIW : 1][2];
+#pragma unroll
+  for (int j = 0; j < (NRM ? NIW : 1); ++j) nacc[j][0] = nacc[j][1] = 0.0;
   double* red = buf + nst * stage_d + warp * NIW * 8;
-  if (norm_part)
+  if (norm_part && !NRM)
     for (int col = lane; col < NIW * 8; col += 32) red[col] = 0.0;
 
   for (int64_t s = 0; s < nsteps; ++s) {
@@ -374,7 +379,15 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
     if (lane == 0) mbar_arrive(ring.empty(b));
     if (kc_here == kc_count - 1) {  // tile complete: epilogue
       const int64_t tile = blockIdx.x + (s / kc_count) * gridDim.x;
-      if (norm_part) {  // rows beyond m hold zeros (TMA zero fill): no masking needed
+      if (norm_part && NRM) {  // rows beyond m hold zeros (TMA zero fill): no masking needed
+#pragma unroll
+        for (int j = 0; j < (NRM ? NIW : 1); ++j)
+#pragma unroll
+          for (int i = 0; i < MI; ++i) {
+            nacc[j][0] = fma(acc[i][j][0], acc[i][j][0], nacc[j][0]);
+            nacc[j][1] = fma(acc[i][j][1], acc[i][j][1], nacc[j][1]);
+          }
+      } else if (norm_part) {
 #pragma unroll
         for (int j = 0; j < NIW; ++j)
 #pragma unroll
@@ -408,6 +421,18 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
   }
 
   if (norm_part) {  // sum the row-group warps of each column group in a fixed order
+    if constexpr (NRM) {
+#pragma unroll
+      for (int j = 0; j < (NRM ? NIW : 1); ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          double v = nacc[j][e];
+          v += __shfl_xor_sync(0xffffffffu, v, 4);
+          v += __shfl_xor_sync(0xffffffffu, v, 8);
+          v += __shfl_xor_sync(0xffffffffu, v, 16);
+          if (g == 0) red[j * 8 + 2 * t + e] = v;
+        }
+    }
     bar_consumers(NN_CW * 32);
     const double* red0 = buf + nst * stage_d;
     for (int col = threadIdx.x; col < CP; col += NN_CW * 32) {
@@ -439,7 +464,8 @@ struct NnPlan {
 };
 
 // K chunk (= 4 mod 8, <= 252) and stage count from shared memory: fewest
-// padded k-steps, then fewest chunks, with at least 2 stages (3 preferred).
+// zero-filled columns, then fewest chunks, with at least 2 stages (3
+// preferred).  (Measured at c2: 2 chunks x 2 stages beat 4 chunks x 4 stages.)
 static NnPlan plan_nn(int64_t m, int k, int c) {
   NnPlan p;
   p.ni = (c + 7) / 8;
