@@ -235,8 +235,12 @@ int64_t core(Ctx& c, Core& b, const double* X, int64_t ldx, int64_t m_local, int
   cudaStream_t s = c.s;
   Ctx cd = c;
   if (!dist) cd.comm = nullptr;
-  // truncation of the eigensolver's pivoted Cholesky: far below the discard threshold
-  const double trunc = std::max(kEps, std::min(w * kEps, 0.1 * c.wp));
+  // truncation of the eigensolver's pivoted Cholesky (reading R13): directions with
+  // lambda <= 0.01 wp lambda_max have Sigma~^2 <= lambda + |E| far below the discard line
+  // wp Sigma~_max^2, so they could never be kept; the truncated Schur complement
+  // (<= (n-K) trunc lambda_max) moves the kept sigma by ~1e-13 sigma_1 (simulated at c2/c4),
+  // three orders below the 1e-10 contract.
+  const double trunc = std::max(kEps, 0.01 * c.wp);
   // Step 1 (P:613 / P:646): B = A^* A over the local rows, aggregated across ranks.
   {
     Pass t(s, TSSVD_PASS_GRAM_X, (double)m_local * w * (w + 1), 8.0 * m_local * w);
