@@ -225,3 +225,35 @@ def test_lowrank_paper_table8_pin():
     assert gpu[1].size == ref[1].size == 6
     err = oracle.spectral_error(a, *gpu, synth.power_start(2_000, 7))
     assert err == pytest.approx(4.83e-07, rel=5e-3)
+
+
+@pytest.mark.slow
+def test_lowrank_c3_full_size_properties():
+    """BASELINE configs[2] at full size (200,000 x 20,000, 32 GB), the `bench.py --config c3`
+    workload.  The oracle cannot run at this size, so check what holds at any size: the
+    leading sigma against the constructed spectrum (Weyl: |d sigma| <= ||noise||_2), the
+    orthonormality of U and V (cuBLAS Gram, independent of our kernels), and the spectral
+    error against sigma_{k+1} of the constructed spectrum (power method, torch)."""
+    d = synth.config_inputs("c3")
+    A = torch.from_numpy(d["A"]).to(DEV)
+    om = torch.from_numpy(d["Omega"]).to(DEV)
+    u, s, v = tk.lowrank_svd(A, om, d["iters"], d["k"])
+    torch.cuda.synchronize()
+    m, n = A.shape
+    k = d["k"]
+    assert s.numel() == k
+    sig = d["sigma"]
+    noise = synth.CONFIGS["c3"]["noise"] * (np.sqrt(m) + np.sqrt(n)) / np.sqrt(n) * 1.1
+    sg = s.cpu().numpy()
+    assert np.all(np.diff(sg) <= 0)
+    assert np.max(np.abs(sg - sig[:k])) <= noise + 1e-10 * sig[0]
+    eye = torch.eye(k, dtype=torch.float64, device=DEV)
+    assert (u.T @ u - eye).abs().max().item() <= 1e-13
+    assert (v.T @ v - eye).abs().max().item() <= 1e-13
+    x = torch.from_numpy(d["x0"]).to(DEV)
+    for _ in range(20):  # power iteration on M^T M, M = A - U S V^T (never formed)
+        y = A @ x - u @ (s * (v.T @ x))
+        x = A.T @ y - v @ (s * (u.T @ y))
+        x = x / x.norm()
+    err = (A @ x - u @ (s * (v.T @ x))).norm().item()
+    assert abs(err - sig[k]) <= 0.01 * sig[k] + noise
