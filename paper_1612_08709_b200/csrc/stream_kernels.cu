@@ -25,6 +25,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 
 #include "common.cuh"
@@ -349,7 +350,7 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
     for (int j = 0; j < NIW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   // per-warp column sums of squares (norm epilogue): in registers over the whole
   // run when they fit (NRM), else per tile into a shared-memory row after the stages
-  constexpr bool NRM = 2 * MI * NIW + 2 * NIW <= 48;
+  constexpr bool NRM = 2 * MI * NIW + 2 * NIW <= 56;  // (measured: no spills up to 56)
   double nacc[NRM ? NIW : 1][2];
 #pragma unroll
   for (int j = 0; j < (NRM ? NIW : 1); ++j) nacc[j][0] = nacc[j][1] = 0.0;
@@ -482,9 +483,11 @@ static NnPlan plan_nn(int64_t m, int k, int c) {
     if (nst < 2) break;
     const int chunks = (int)ceil_div(k, kc);
     const double waste = (double)(chunks * kc - k) / k;
-    const double score = waste + 0.01 * chunks + (nst < 3 ? 0.05 : 0.0);
+    const double score = waste + chunks / (double)k + (nst < 3 ? 0.05 : (nst < 4 ? 0.02 : 0.0));
     if (score < best) best = score, p.KC = kc;
   }
+  static const int force_kc = getenv("TSSVD_NN_KC") ? atoi(getenv("TSSVD_NN_KC")) : 0;  // experiments
+  if (force_kc >= 28 && force_kc % 8 == 4) p.KC = force_kc;
   p.kcc = (int)ceil_div(k, p.KC);
   const size_t stage = (size_t)(p.R * p.KC + p.KC * p.ldm) * 8;
   p.nst = (int)std::max<size_t>(2, std::min<size_t>(8, budget / stage));
