@@ -91,6 +91,30 @@ __device__ __forceinline__ void warp_argmax(double& v, int& i) {
   }
 }
 
+// DSMEM producer/consumer exchange: remote shared address of `p` in CTA `rank`,
+// st.async of one double that signals the remote mbarrier's transaction count.
+__device__ __forceinline__ uint32_t mapa_u32(const void* p, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];\n" ::"r"(raddr),
+               "l"(__double_as_longlong(v)), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // Reciprocal and reciprocal square root: MUFU approximation + two Newton steps.
 __device__ __forceinline__ double rcp_nr(double x) {
   double y;
@@ -121,9 +145,15 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
   __shared__ double s_nrm[JMAX];
   __shared__ double s_cand[4][2];  // C > 1: per-CTA pivot candidates (value, index)
   __shared__ double s_red[JW];
+  __shared__ __align__(8) uint64_t s_xbar[2];  // C > 1: per-round-parity exchange barriers
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long t_start = clock64();
+  if (C > 1 && tid == 0) {
+    mbar_init(&s_xbar[0], 1);
+    mbar_init(&s_xbar[1], 1);
+    fence_mbar_init();
+  }
   const int nslots = a.mode == 0 ? a.n : a.N;
   const int P = a.P, Lh = a.Lh;
   const int row0 = h * Lh;                         // first global row held here
@@ -173,9 +203,10 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
     cl.sync();
 
     bool done = false;
-    if constexpr (C == 1) {
+    {
       if (n <= 128) {
         // ---- diagonally pivoted Cholesky with the Schur complement in registers ----
+        // (every CTA of a cluster runs it redundantly -- bit-identical -- and keeps its rows)
         // Thread (warp w, lane l) owns S[r][c] for rows r = l + 32 i (i < 4) and
         // slots c = w + 16 j (j < 8).  Step k with pivot p: the owner warp of
         // slot p publishes column p (pcol) and writes X[:, k] = pcol / sqrt(S_pp)
@@ -190,7 +221,7 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int c = warp + JW * j, r = lane + 32 * i;
-            Sr[j][i] = (c < n && r < n) ? X[c * P + r] : 0.0;
+            Sr[j][i] = (c < n && r < n) ? a.in[(size_t)c * a.ldin + r] : 0.0;  // B symmetric
           }
         // diagonal element r (r = lane + 32 i) lives in slot j = r / 16 of warp r % 16
 #pragma unroll
@@ -230,7 +261,7 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
               for (int j = 0; j < 8; ++j) v = j == jp ? Sr[j][i] : v;
               if (r < n) {
                 pcol[r] = v;
-                X[k * P + r] = ((rmask >> i) & 1) ? 0.0 : v * rsq;
+                if (r >= row0 && r < row0 + nloc) X[k * P + (r - row0)] = ((rmask >> i) & 1) ? 0.0 : v * rsq;
               }
             }
           }
@@ -466,15 +497,27 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
         }
       }
       if constexpr (C > 1) {
-        double* xb = xch + ((size_t)(rounds & 1) * JMAXP + (has ? gidx : 0)) * C * 4;
-        if (has && gl == 0)
+        // partial dot products to every CTA of the cluster: plain stores locally, st.async
+        // to the peers (completing their per-parity exchange mbarrier), then wait for the
+        // C-1 remote contributions; summed in CTA order (identical on every CTA)
+        const int par = rounds & 1;
+        uint64_t* xbar = &s_xbar[par];
+        double* xb = xch + ((size_t)par * JMAXP + (has ? gidx : 0)) * C * 4;
+        if (tid == 0) mbar_arrive_expect_tx(xbar, (uint32_t)((C - 1) * npairs * 24));
+        if (has && gl == 0) {
+          xb[h * 4] = al;
+          xb[h * 4 + 1] = be;
+          xb[h * 4 + 2] = ga;
           for (int qc = 0; qc < C; ++qc) {
-            double* d = cl.at(xb, qc) + h * 4;
-            d[0] = al;
-            d[1] = be;
-            d[2] = ga;
+            if (qc == h) continue;
+            const uint32_t rb = mapa_u32(xbar, qc), rx = mapa_u32(xb + h * 4, qc);
+            st_async_f64(rx, al, rb);
+            st_async_f64(rx + 8, be, rb);
+            st_async_f64(rx + 16, ga, rb);
           }
-        cl.sync();
+        }
+        __syncthreads();  // local contributions visible
+        mbar_wait_cluster(xbar, (uint32_t)((rounds >> 1) & 1));
         al = be = ga = 0.0;
         for (int qc = 0; qc < C; ++qc) al += xb[qc * 4], be += xb[qc * 4 + 1], ga += xb[qc * 4 + 2];
       }
@@ -601,8 +644,8 @@ static size_t jac_smem(int C, int nslots, int P) {
 // Round cost model (cycles; B200 measured: DFMA/DADD 7-cycle latency, 2 issue
 // cycles per warp-instruction on the 16-lane FP64 unit, SHFL+DADD 35, LDS 29,
 // shared-memory bandwidth 128 B/cycle/SM, MUFU f64 ~19; the rotation
-// parameters ~230 on the critical path; a cluster round (DSMEM exchange +
-// barrier with its membar) ~2500).  A round reads and writes both columns of
+// parameters ~230 on the critical path; a cluster round adds an st.async
+// exchange through DSMEM and an mbarrier wait, ~500).  A round reads and writes both columns of
 // every pair, so one CTA is shared-memory-bandwidth bound.
 static double jac_round_cost(int C, int G, int V, int npairs) {
   const int warps = (int)ceil_div(npairs, 32 / G);
@@ -612,7 +655,7 @@ static double jac_round_cost(int C, int G, int V, int npairs) {
   const double pipe = 2.0 * per_smsp * (14.0 * V + 3.0 * lg + 35.0);
   const double smem = 2.0 * npairs * (2.0 * G * V) * 16.0 / 128.0 / C;
   const double chain = 60.0 + 9.0 * V + 35.0 * lg + 230.0 + 16.0 * V;
-  return std::max(pipe, smem) + chain + (C > 1 ? 2500.0 : 50.0);
+  return std::max(pipe, smem) + chain + (C > 1 ? 500.0 : 50.0);
 }
 
 static cudaError_t jac_dispatch(JacArgs a, cudaStream_t s) {
