@@ -12,14 +12,15 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 
 template <int MI, int NI>
 __global__ void k(double* out, int iters) {
-  __shared__ double s[64 * 36];
-  for (int i = threadIdx.x; i < 64 * 36; i += blockDim.x) s[i] = 1.0 + i * 1e-9;
+  __shared__ double s[2 * 64 * 36];
+  for (int i = threadIdx.x; i < 2 * 64 * 36; i += blockDim.x) s[i] = 1.0 + i * 1e-9;
   __syncthreads();
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   double acc[MI][NI][2] = {};
-  const double* xa = s + g * 36 + t;
-  const double* xb = s + t * 36 + g;
   for (int it = 0; it < iters; ++it) {
+    // the stage alternates between two buffers: the loads cannot be hoisted
+    const double* xa = s + (it & 1) * 64 * 36 + g * 36 + t;
+    const double* xb = s + (it & 1) * 64 * 36 + t * 36 + g;
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
       double a[MI], b[NI];
@@ -44,14 +45,14 @@ __global__ void k(double* out, int iters) {
 // the gemm_nn inner loop shape: runtime k-step count per stage, 13 k-steps
 template <int MI, int NI>
 __global__ void k_rt(double* out, int iters, int nks) {
-  __shared__ double s[64 * 36];
-  for (int i = threadIdx.x; i < 64 * 36; i += blockDim.x) s[i] = 1.0 + i * 1e-9;
+  __shared__ double s[2 * 64 * 36];
+  for (int i = threadIdx.x; i < 2 * 64 * 36; i += blockDim.x) s[i] = 1.0 + i * 1e-9;
   __syncthreads();
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   double acc[MI][NI][2] = {};
-  const double* xa = s + g * 36 + t;
-  const double* xb = s + t * 36 + g;
   for (int it = 0; it < iters; ++it) {
+    const double* xa = s + (it & 1) * 64 * 36 + g * 36 + t;
+    const double* xb = s + (it & 1) * 64 * 36 + t * 36 + g;
     for (int kk = 0; kk < nks; ++kk) {
       double a[MI];
 #pragma unroll
@@ -117,5 +118,8 @@ int main() {
   run_rt<3, 7>(out, 8, sms, 7);
   for (int w : {4, 8, 12, 16}) run<2, 10>(out, w, sms);
   for (int w : {8, 16}) run<3, 7>(out, w, sms);
+  for (int w : {8, 16, 24, 32}) run<2, 2>(out, w, sms);
+  for (int w : {8, 16}) run<4, 4>(out, w, sms);
+  for (int w : {8, 16, 28}) run<1, 7>(out, w, sms);
   return 0;
 }
