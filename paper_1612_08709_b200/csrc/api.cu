@@ -109,7 +109,16 @@ struct Ctx {
   cudaStream_t s = nullptr;
   double wp = 1e-11;
   int max_sweeps = 60;
+  // Jacobi solves whose convergence is checked after the call's final sync
+  // (no host round trip per solve): device info slots of 8 ints each
+  int* jinfo = nullptr;
+  int njinfo = 0;
+  static constexpr int kMaxDeferred = 48;
   bool dist() const { return comm && comm->nranks > 1; }
+  int* next_info() {
+    if (njinfo >= kMaxDeferred) fail(TSSVD_ECUDA, "too many deferred Jacobi solves");
+    return jinfo + 8 * njinfo++;
+  }
 };
 
 void allreduce(Ctx& c, double* buf, int64_t count) {
@@ -202,22 +211,38 @@ struct Core {
   }
 };
 
-int jacobi_info(Ctx& c, Core& b, const char* what, int N) {
+int jacobi_info(Ctx& c, const int* info, const char* what, int N) {
   int h[3];
-  read_ints(c, b.info, 3, h);
+  read_ints(c, info, 3, h);
   if (g_stats.n_jacobi < 16) g_stats.jacobi_sweeps[g_stats.n_jacobi++] = h[0];
   if (!h[1]) fail(TSSVD_ENOCONV, "Jacobi %s (N=%d) not converged in %d sweeps", what, N, h[0]);
   return h[2];
 }
 
+// After the final sync of a call: every deferred solve must have converged.
+void check_deferred(Ctx& c) {
+  if (!c.njinfo) return;
+  static thread_local int* h = nullptr;
+  if (!h) CU(cudaHostAlloc(reinterpret_cast<void**>(&h), 8 * Ctx::kMaxDeferred * sizeof(int), cudaHostAllocDefault));
+  CU(cudaMemcpyAsync(h, c.jinfo, 8 * c.njinfo * sizeof(int), cudaMemcpyDeviceToHost, c.s));
+  CU(cudaStreamSynchronize(c.s));
+  for (int q = 0; q < c.njinfo; ++q) {
+    if (g_stats.n_jacobi < 16) g_stats.jacobi_sweeps[g_stats.n_jacobi++] = h[8 * q];
+    if (!h[8 * q + 1]) fail(TSSVD_ENOCONV, "Jacobi solve %d not converged in %d sweeps", q, h[8 * q]);
+  }
+}
+
 // Eigendecomposition of the PSD matrix B (n x n, ld n) in place: returns k and
 // leaves eigenvector j (unit, descending eigenvalue) at B + j*n.  Pivots below
 // trunc_rel * max diag are dropped (numerically null directions; reading R10).
-int eig(Ctx& c, Core& b, double* B, int n, double* vals, double trunc_rel) {
+// sync = false: no host round trip -- returns n (the kernel zero-fills the
+// eigenvector slots [k, n), which then carry zero norms into the next discard)
+// and convergence is checked after the call.
+int eig(Ctx& c, Core& b, double* B, int n, double* vals, double trunc_rel, bool sync = true) {
   Pass t(c.s, TSSVD_PASS_JACOBI, 0, 0);
-  KL(launch_jacobi_eig(B, n, n, std::max(n, 8) * kEps, trunc_rel, c.max_sweeps, B, n, vals,
-                       b.info, c.s));
-  return jacobi_info(c, b, "eig", n);
+  int* info = sync ? b.info : c.next_info();
+  KL(launch_jacobi_eig(B, n, n, std::max(n, 8) * kEps, trunc_rel, c.max_sweeps, B, n, vals, info, c.s));
+  return sync ? jacobi_info(c, info, "eig", n) : n;
 }
 
 void note_rank(int64_t r) {
@@ -300,8 +325,7 @@ int64_t core(Ctx& c, Core& b, const double* X, int64_t ldx, int64_t m_local, int
   }
   KS(build_z(b.G, nc, b.idx, b.sig, r, b.Z, s));
   // Step 8: Z = W D W^*  (W: r x kz, column-major in b.Z).
-  const int kz = eig(c, b, b.Z, r, b.dz, trunc);
-  if (kz == 0) fail(TSSVD_ENONFINITE, "Gram matrix of Y is zero");
+  const int kz = eig(c, b, b.Z, r, b.dz, trunc, false);  // Z = Y^T Y ~ I: kz = r
   // Steps 9-10: Q~ = Y W, T = column norms of Q~ (norms only, nothing stored).
   const int ldm_k = smem_ld(kz);
   KS(fill(b.M, (int64_t)mrows_for(nc) * ldm_k, 0.0, s));
@@ -325,8 +349,7 @@ int64_t core(Ctx& c, Core& b, const double* X, int64_t ldx, int64_t m_local, int
   {
     Pass t(s, TSSVD_PASS_JACOBI, 0, 0);
     KL(launch_jacobi_svd(b.Rt, r2, r, r2, std::max(r2, 8) * kEps, c.max_sweeps, b.Rt + (size_t)r2 * r,
-                         r2 + r, b.sv, b.info, s));
-    jacobi_info(c, b, "svd", r);
+                         r2 + r, b.sv, c.next_info(), s));
   }
   KS(svd_out(b.Rt + (size_t)r2 * r, r2 + r, r2, r, b.sv, b.B, w, b.idx, sigma, V, ldv, b.Ps, s));
   // Step 15: U = Q P = Y~[:, :nc] (S W T^-1 P), in place.
@@ -371,6 +394,7 @@ int64_t global_rows(Ctx& c, int64_t m_local, void* scratch_dev) {
 
 struct TsPlan {
   Core core;
+  int* jinfo;
   int64_t* m_scratch;
   double* a_stage;  // host_io: device copy of A (also holds Y~)
   double* u_pack;   // host_io: U packed (ld (r+1)&~1) for one contiguous D2H copy
@@ -379,6 +403,7 @@ struct TsPlan {
 };
 
 size_t plan_tssvd(Arena& a, TsPlan& p, int64_t m_local, int n, const tssvd_opts* o) {
+  p.jinfo = a.get<int>(8 * Ctx::kMaxDeferred);
   p.m_scratch = a.get<int64_t>(2);
   p.core.alloc(a, m_local, n);
   if (o && o->host_io) {
@@ -427,6 +452,7 @@ void tssvd_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, cons
   a.dry = false;
   TsPlan p;
   plan_tssvd(a, p, m_local, (int)n, opts);
+  c.jinfo = p.jinfo;
   const int64_t m = global_rows(c, m_local, p.m_scratch);
   if (m < n) fail(TSSVD_EINVAL, "m = %lld < n = %lld (the matrix must be tall, P:98-104)", (long long)m, (long long)n);
   const double* X = A;
@@ -463,6 +489,7 @@ void tssvd_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, cons
     CU(cudaMemcpy2DAsync(V, ldv * 8, Vd, ldvd * 8, r * 8, n, cudaMemcpyDeviceToHost, c.s));
   }
   CU(cudaStreamSynchronize(c.s));
+  check_deferred(c);
   g_timer.resolve();
   *rank = r;
 }
@@ -470,6 +497,7 @@ void tssvd_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, cons
 // ------------------------------------------------------------- low rank --
 struct LrPlan {
   Core tall, small;
+  int* jinfo;
   int64_t* m_scratch;
   double *Qt, *Y, *Z, *tn, *Ut, *sig_tmp, *v_scr, *sig_scr, *Mfin;
   double *a_stage, *o_stage, *u_stage, *s_stage, *vo_stage;
@@ -479,6 +507,7 @@ struct LrPlan {
 size_t plan_lowrank(Arena& a, LrPlan& p, int64_t m_local, int n, int l, const tssvd_opts* o) {
   p.lp = (l + 1) & ~1;
   p.ldzmax = pad8(l);
+  p.jinfo = a.get<int>(8 * Ctx::kMaxDeferred);
   p.m_scratch = a.get<int64_t>(2);
   p.tall.alloc(a, m_local, l);
   p.small.alloc(a, n, l);
@@ -547,6 +576,7 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
   a.dry = false;
   LrPlan p;
   plan_lowrank(a, p, m_local, (int)n, (int)l, opts);
+  c.jinfo = p.jinfo;
   const int64_t m = global_rows(c, m_local, p.m_scratch);
   if (l >= std::min<int64_t>(m, n)) fail(TSSVD_EINVAL, "need l < min(m, n) (P:705-707)");
   const int N = (int)n, Lc = (int)l;
@@ -575,12 +605,12 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
     ++g_stats.a_passes;
     // step 4: Y_j = Q_j R_j by Alg. 3 (Q_j = U, in place in Y)
     const int64_t r = core(c, p.tall, p.Y, p.lp, m_local, lj, 1, true, p.Y, p.lp, p.sig_scr, p.v_scr, lj);
-    if (r == 0) { *rank = 0; CU(cudaStreamSynchronize(c.s)); return; }
+    if (r == 0) { *rank = 0; CU(cudaStreamSynchronize(c.s)); check_deferred(c); return; }
     // step 5: Y~_j = A^* Q_j
     const int ldz = tn_pass(c, p, Ad, ldad, m_local, N, (int)r);
     // step 6: Y~_j = Q~_j R~_j by Alg. 3 on the replicated n x r matrix
     const int64_t r2 = core(c, p.small, p.Z, ldz, N, (int)r, 1, false, p.Z, ldz, p.sig_scr, p.v_scr, r);
-    if (r2 == 0) { *rank = 0; CU(cudaStreamSynchronize(c.s)); return; }
+    if (r2 == 0) { *rank = 0; CU(cudaStreamSynchronize(c.s)); check_deferred(c); return; }
     lj = (int)r2;
     KS(rows_to_m(p.Z, ldz, N, lj, p.Qt, smem_ld(lj), mrows_for(N), c.s));
   }
@@ -591,12 +621,12 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
   }
   ++g_stats.a_passes;
   const int64_t r3 = core(c, p.tall, p.Y, p.lp, m_local, lj, 2, true, p.Y, p.lp, p.sig_scr, p.v_scr, lj);
-  if (r3 == 0) { *rank = 0; CU(cudaStreamSynchronize(c.s)); return; }
+  if (r3 == 0) { *rank = 0; CU(cudaStreamSynchronize(c.s)); check_deferred(c); return; }
   // Alg. 6 step 1: B^T = A^* Q
   const int ldz = tn_pass(c, p, Ad, ldad, m_local, N, (int)r3);
   // Alg. 6 step 2: B^T = V Sigma U~^* by Alg. 4 (reading R6); V in place in Z
   const int64_t r4 = core(c, p.small, p.Z, ldz, N, (int)r3, 2, false, p.Z, ldz, p.sig_tmp, p.Ut, Lc);
-  if (r4 == 0) { *rank = 0; CU(cudaStreamSynchronize(c.s)); return; }
+  if (r4 == 0) { *rank = 0; CU(cudaStreamSynchronize(c.s)); check_deferred(c); return; }
   KS(canon_lowrank(p.Z, ldz, N, p.Ut, Lc, (int)r3, (int)r4, c.s));
   const int kk = (int)std::min<int64_t>(k, r4);
   // Alg. 6 step 3: U = Q U~ (leading kk columns, reading R7)
@@ -620,6 +650,7 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
     CU(cudaMemcpy2DAsync(V, ldv * 8, Vo, ldvo * 8, kk * 8, N, cudaMemcpyDeviceToHost, c.s));
   }
   CU(cudaStreamSynchronize(c.s));
+  check_deferred(c);
   g_timer.resolve();
   *rank = kk;
 }

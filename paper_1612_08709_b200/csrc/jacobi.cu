@@ -582,6 +582,12 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
     }
     if (lane == 0 && h == 0) a.vals[rk] = a.mode == 0 ? n2 : nj;
   }
+  if (a.mode == 0)  // eigenvector slots [K, n) are zero (callers may use all n without reading K)
+    for (int e = tid; e < (a.n - K) * nloc; e += JT) {
+      const int kk = K + e / nloc, r = e % nloc;
+      a.out[(size_t)kk * a.ldout + row0 + r] = 0.0;
+      if (r == 0 && h == 0) a.vals[kk] = 0.0;
+    }
   if (h == 0 && tid == 0) {
     a.info[0] = sweep;
     a.info[1] = converged ? 1 : 0;
@@ -645,7 +651,9 @@ static size_t jac_smem(int C, int nslots, int P) {
 // cycles per warp-instruction on the 16-lane FP64 unit, SHFL+DADD 35, LDS 29,
 // shared-memory bandwidth 128 B/cycle/SM, MUFU f64 ~19; the rotation
 // parameters ~230 on the critical path; a cluster round adds an st.async
-// exchange through DSMEM and an mbarrier wait, ~500).  A round reads and writes both columns of
+// exchange through DSMEM and an mbarrier wait: measured ~1400 more than the
+// shared-memory traffic it saves, so clusters only when one CTA cannot hold
+// the columns).  A round reads and writes both columns of
 // every pair, so one CTA is shared-memory-bandwidth bound.
 static double jac_round_cost(int C, int G, int V, int npairs) {
   const int warps = (int)ceil_div(npairs, 32 / G);
@@ -655,7 +663,7 @@ static double jac_round_cost(int C, int G, int V, int npairs) {
   const double pipe = 2.0 * per_smsp * (14.0 * V + 3.0 * lg + 35.0);
   const double smem = 2.0 * npairs * (2.0 * G * V) * 16.0 / 128.0 / C;
   const double chain = 60.0 + 9.0 * V + 35.0 * lg + 230.0 + 16.0 * V;
-  return std::max(pipe, smem) + chain + (C > 1 ? 500.0 : 50.0);
+  return std::max(pipe, smem) + chain + (C > 1 ? 1400.0 : 50.0);  // cluster: calibrated on B200
 }
 
 static cudaError_t jac_dispatch(JacArgs a, cudaStream_t s) {
