@@ -39,6 +39,7 @@ def parse():
     p.add_argument("--wp", type=float, default=1e-11)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-clocks", action="store_true", help="diagnosis: no clock sampling")
     p.add_argument("--cpu-sample-rows", type=int, default=0)
     return p.parse_args()
 
@@ -188,7 +189,8 @@ def run_ours(args, rank, world, local_rank):
     launches = st["kernel_launches"]
     barrier()
     clocks = Clocks(local_rank)
-    clocks.start()
+    if not args.no_clocks:
+        clocks.start()
     _lib.set_pass_timing(True)
     pass_ms = {}
     pass_flops = {}

@@ -231,14 +231,42 @@ __global__ void k_build_m2(const double* W, int r, const int* idx, const double*
 
 // Low-rank final step: flip (V_A[:, a], Ut(:, a)) so V_A's largest entry is positive (R5),
 // V_A row-major (n x ?, ldva), Ut row-major (r3 x r4, ldu_t).  One thread per column.
-__global__ void k_canon_lowrank(double* VA, int64_t ldva, int n, double* Ut, int ldut, int r3,
-                                int r4) {
-  const int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a >= r4) return;
-  const double sg = col_sign(VA + a, (int)ldva, n);
-  if (sg < 0) {
-    for (int i = 0; i < n; ++i) VA[(size_t)i * ldva + a] = -VA[(size_t)i * ldva + a];
-    for (int i = 0; i < r3; ++i) Ut[(size_t)i * ldut + a] = -Ut[(size_t)i * ldut + a];
+__global__ void __launch_bounds__(256) k_canon_lowrank(double* VA, int64_t ldva, int n, double* Ut, int ldut,
+                                                        int r3, int r4) {
+  // one CTA per column a: block argmax of |V_A(:, a)| (ties -> lowest row), then a parallel flip
+  __shared__ double sv[8];
+  __shared__ int si[8];
+  __shared__ double sgn;
+  const int a = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double bv = -1.0, val = 0.0;
+  int bi = 1 << 30;
+  for (int i = tid; i < n; i += blockDim.x) {
+    const double v = VA[(size_t)i * ldva + a];
+    if (fabs(v) > bv) bv = fabs(v), bi = i, val = v;  // increasing i: ties keep the lowest
+  }
+  double sv_ = val < 0.0 ? -1.0 : 1.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    const double os = __shfl_xor_sync(0xffffffffu, sv_, o);
+    if (ob > bv || (ob == bv && oi < bi)) bv = ob, bi = oi, sv_ = os;
+  }
+  if (lane == 0) sv[warp] = bv, si[warp] = bi;
+  __shared__ double ss[8];
+  if (lane == 0) ss[warp] = sv_;
+  __syncthreads();
+  if (tid == 0) {
+    double b = -1.0, g = 1.0;
+    int i0 = 1 << 30;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+      if (sv[w] > b || (sv[w] == b && si[w] < i0)) b = sv[w], i0 = si[w], g = ss[w];
+    sgn = g;
+  }
+  __syncthreads();
+  if (sgn < 0) {
+    for (int i = tid; i < n; i += blockDim.x) VA[(size_t)i * ldva + a] = -VA[(size_t)i * ldva + a];
+    for (int i = tid; i < r3; i += blockDim.x) Ut[(size_t)i * ldut + a] = -Ut[(size_t)i * ldut + a];
   }
 }
 
@@ -302,7 +330,7 @@ void build_m2(const double* W, int r, const int* idx, const double* sig, const d
 }
 void canon_lowrank(double* VA, int64_t ldva, int n, double* Ut, int ldut, int r3, int r4,
                    cudaStream_t s) {
-  k_canon_lowrank<<<nb(r4, 64), 64, 0, s>>>(VA, ldva, n, Ut, ldut, r3, r4);
+  if (r4 > 0) k_canon_lowrank<<<r4, 256, 0, s>>>(VA, ldva, n, Ut, ldut, r3, r4);
 }
 void copy2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int cols,
             cudaStream_t s) {

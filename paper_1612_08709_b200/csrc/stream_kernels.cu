@@ -289,10 +289,31 @@ __global__ void reduce_parts_kernel(const double* __restrict__ part, int np, int
   if (lane == 0) out[e] = v;
 }
 
+// Long outputs (the n x l partials of A^T Q): one thread per element, partials
+// summed in a fixed two-level order (groups of ~sqrt(np)), coalesced over e.
+__global__ void reduce_parts_long_kernel(const double* __restrict__ part, int np, int64_t stride,
+                                         int64_t len, double* __restrict__ out) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= len) return;
+  int gs = 1;
+  while (gs * gs < np) ++gs;
+  double tot = 0.0;
+  for (int p0 = 0; p0 < np; p0 += gs) {
+    double s = 0.0;
+    const int p1 = min(np, p0 + gs);
+    for (int q = p0; q < p1; ++q) s += part[(size_t)q * stride + e];
+    tot += s;
+  }
+  out[e] = tot;
+}
+
 cudaError_t launch_reduce_parts(const double* part, int np, int64_t stride, int64_t len,
                                 double* out, cudaStream_t s) {
   if (len <= 0) return cudaSuccess;
-  reduce_parts_kernel<<<(int)ceil_div(len * 32, 256), 256, 0, s>>>(part, np, stride, len, out);
+  if (len >= 32768)
+    reduce_parts_long_kernel<<<(int)ceil_div(len, 256), 256, 0, s>>>(part, np, stride, len, out);
+  else
+    reduce_parts_kernel<<<(int)ceil_div(len * 32, 256), 256, 0, s>>>(part, np, stride, len, out);
   return cudaGetLastError();
 }
 
