@@ -667,14 +667,16 @@ TnPlan plan_gemm_tn(int64_t m, int n, int l) {
   while (p.kr > 8 && 3 * p.kr * row_bytes > budget) p.kr -= 8;
   p.nst = (int)std::min<size_t>(8, budget / (p.kr * row_bytes));
   const int sms = dev_info().sms;
-  // split count: best wave efficiency, at least 256 rows per split
+  // split count: wave efficiency x per-CTA amortisation (a CTA's prologue -- ring
+  // set-up, first TMA round trip -- and partial write cost ~20 stages, measured)
   int best = 1;
   double best_eff = -1;
   for (int s = 1; s <= 64; ++s) {
     if (s > 1 && ceil_div(m, s) < 256) break;
     const int64_t tot = (int64_t)p.colblocks * s;
     const double eff = (double)tot / (double)(ceil_div(tot, sms) * sms);
-    const double score = eff * std::min(1.0, (double)tot / sms);
+    const double steps = (double)ceil_div(ceil_div(m, s), p.kr);
+    const double score = eff * std::min(1.0, (double)tot / sms) * steps / (steps + 20.0);
     if (score > best_eff + 1e-9) best_eff = score, best = s;
   }
   p.splits = best;
