@@ -232,6 +232,12 @@ void check_deferred(Ctx& c) {
   }
 }
 
+// One-sided Jacobi rotation threshold for columns of `rows` dot-product rows:
+// |x_p.x_q| > tol |x_p||x_q|, tol = max(8, 2 sqrt(rows)) eps -- LAPACK dgesvj's
+// sqrt(M) eps with a factor 2 of margin over the dot products' rounding noise (an
+// n eps threshold let the orthonormality of U drift to 1.1e-13 at r = 128).
+inline double jacobi_tol(int rows) { return std::max(8.0, 2.0 * std::sqrt((double)rows)) * kEps; }
+
 // Eigendecomposition of the PSD matrix B (n x n, ld n) in place: returns k and
 // leaves eigenvector j (unit, descending eigenvalue) at B + j*n.  Pivots below
 // trunc_rel * max diag are dropped (numerically null directions; reading R10).
@@ -241,7 +247,7 @@ void check_deferred(Ctx& c) {
 int eig(Ctx& c, Core& b, double* B, int n, double* vals, double trunc_rel, bool sync = true) {
   Pass t(c.s, TSSVD_PASS_JACOBI, 0, 0);
   int* info = sync ? b.info : c.next_info();
-  KL(launch_jacobi_eig(B, n, n, std::max(n, 8) * kEps, trunc_rel, c.max_sweeps, B, n, vals, info, c.s));
+  KL(launch_jacobi_eig(B, n, n, jacobi_tol(n), trunc_rel, c.max_sweeps, B, n, vals, info, c.s));
   return sync ? jacobi_info(c, info, "eig", n) : n;
 }
 
@@ -348,7 +354,7 @@ int64_t core(Ctx& c, Core& b, const double* X, int64_t ldx, int64_t m_local, int
   KS(build_k(b.T, b.idx2, r2, b.Z, r, b.sig, b.idx, b.Rt, s));
   {
     Pass t(s, TSSVD_PASS_JACOBI, 0, 0);
-    KL(launch_jacobi_svd(b.Rt, r2, r, r2, std::max(r2, 8) * kEps, c.max_sweeps, b.Rt + (size_t)r2 * r,
+    KL(launch_jacobi_svd(b.Rt, r2, r, r2, jacobi_tol(r2), c.max_sweeps, b.Rt + (size_t)r2 * r,
                          r2 + r, b.sv, c.next_info(), s));
   }
   KS(svd_out(b.Rt + (size_t)r2 * r, r2 + r, r2, r, b.sv, b.B, w, b.idx, sigma, V, ldv, b.Ps, s));
@@ -873,7 +879,7 @@ int tssvd_sym_eig(void* stream, int64_t n, const double* B, int64_t ldb, double*
     fill(lambda, n, 0.0, s);
     CU(cudaGetLastError());
     // no truncation beyond the noise floor: trunc = eps
-    CU(launch_jacobi_eig(B, (int)ldb, (int)n, std::max<int64_t>(n, 8) * kEps, kEps, max_sweeps,
+    CU(launch_jacobi_eig(B, (int)ldb, (int)n, jacobi_tol((int)n), kEps, max_sweeps,
                          vecs, (int)n, lambda, info, s));
     copy2d(vecs, n, Vt, ldv, n, (int)n, s);  // eigenvector j (contiguous) -> row j of Vt
     CU(cudaGetLastError());

@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
   __shared__ int s_order[JMAX];  // column k -> slot (EIG: pivot order)
   __shared__ int s_rank[JMAX];
   __shared__ double s_nrm[JMAX];
-  __shared__ double s_cand[4][2];  // C > 1: per-CTA pivot candidates (value, index)
+  __shared__ double s_cand[8][2];  // C > 1: per-CTA pivot candidates (value, index)
   __shared__ double s_red[JW];
   __shared__ __align__(8) uint64_t s_xbar[2];  // C > 1: per-round-parity exchange barriers
 
@@ -677,7 +677,7 @@ static cudaError_t jac_dispatch(JacArgs a, cudaStream_t s) {
   static const int force_c = getenv("TSSVD_JAC_C") ? atoi(getenv("TSSVD_JAC_C")) : 0;
   double best = 1e300;
   int bC = 0, bG = 0, bV = 0, bLh = 0;
-  for (int C = 1; C <= 4; C *= 2) {
+  for (int C = 1; C <= 8; C *= 2) {  // 8 = portable cluster limit (SVD of up to 256 x 256)
     const int Lh = (int)((ceil_div(a.L, C) + 1) & ~1);
     for (int G = 4; G <= 16; G *= 2) {
       if (JW * (32 / G) < npairs) continue;  // one pass over the pairs
@@ -697,7 +697,8 @@ static cudaError_t jac_dispatch(JacArgs a, cudaStream_t s) {
   const size_t smem = jac_smem(bC, nslots, a.P);
   if (bC == 1) return jac_g<1>(a, bG, smem, s);
   if (bC == 2) return jac_g<2>(a, bG, smem, s);
-  return jac_g<4>(a, bG, smem, s);
+  if (bC == 4) return jac_g<4>(a, bG, smem, s);
+  return jac_g<8>(a, bG, smem, s);
 }
 
 cudaError_t launch_jacobi_eig(const double* B, int ldb, int n, double tol, double trunc,

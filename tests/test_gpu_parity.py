@@ -257,3 +257,39 @@ def test_lowrank_c3_full_size_properties():
         x = x / x.norm()
     err = (A @ x - u @ (s * (v.T @ x))).norm().item()
     assert abs(err - sig[k]) <= 0.01 * sig[k] + noise
+
+
+def test_building_blocks_with_empty_shard():
+    """A rank of a multi-GPU job may own no rows: every streaming kernel must return zeros
+    (the partials it contributes to the allreduce) rather than fail or read out of bounds."""
+    x = torch.empty((0, 40), dtype=torch.float64, device=DEV)
+    g = tk.gram(x)
+    assert torch.count_nonzero(g).item() == 0
+    y, nsq = tk.matmul(x, torch.ones((40, 12), dtype=torch.float64, device=DEV), norms=True)
+    assert y.shape == (0, 12) and torch.count_nonzero(nsq).item() == 0
+
+
+def test_lowrank_host_io_matches_device():
+    d = synth.config_inputs("c3", m=5_000, n=1_000)
+    a = torch.from_numpy(d["A"])
+    om = torch.from_numpy(d["Omega"])
+    uh, sh, vh = tk.lowrank_svd(a.pin_memory(), om.pin_memory(), d["iters"], d["k"])
+    ud, sd, vd = tk.lowrank_svd(a.to(DEV), om.to(DEV), d["iters"], d["k"])
+    assert torch.equal(sh, sd.cpu()) and torch.equal(vh, vd.cpu()) and torch.equal(uh, ud.cpu())
+
+
+@pytest.mark.parametrize("n", [2, 8, 30, 128, 200, 256])
+def test_tssvd_square(n):
+    """m = n (square, the smallest tall case) with a constructed, well-separated spectrum
+    (sigma geometric 1 -> 1e-3, Haar U and V): Alg. 4 must return the oracle's sigma, U and V
+    within the R12 bound and orthonormal U, V (the r = 128, 200 cases exercise the
+    sqrt(rows) eps rotation threshold and, at 200, the cluster eigensolver)."""
+    rng = np.random.default_rng(100 + n)
+    u, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    sig = 10.0 ** (-3.0 * np.arange(n) / max(n - 1, 1))
+    a = (u * sig) @ v.T
+    gpu = run_tssvd(a, 1e-11, 2)
+    ref = oracle.tssvd(a, 1e-11, 2)
+    assert_tssvd_parity(gpu, ref, passes=2)
+    assert np.max(np.abs(gpu[1] - sig)) <= 1e-12
