@@ -293,3 +293,38 @@ def test_tssvd_square(n):
     ref = oracle.tssvd(a, 1e-11, 2)
     assert_tssvd_parity(gpu, ref, passes=2)
     assert np.max(np.abs(gpu[1] - sig)) <= 1e-12
+
+
+def test_tssvd_strided_lda():
+    """A is a column slice of a wider row-major buffer (lda = n + 6): the TMA tensor maps
+    read rows with the caller's leading dimension."""
+    d = synth.config_inputs("c2", m=50_000)
+    a = d["A"]
+    wide = np.zeros((a.shape[0], a.shape[1] + 6))
+    wide[:, :a.shape[1]] = a
+    W = torch.from_numpy(wide).to(DEV)
+    u, s, v = tk.tssvd(W[:, :a.shape[1]], wp=1e-11, passes=2)
+    torch.cuda.synchronize()
+    ref = oracle.tssvd(a, 1e-11, 2)
+    assert_tssvd_parity((u.cpu().numpy(), s.cpu().numpy(), v.cpu().numpy()), ref, passes=2)
+
+
+def test_lowrank_l128():
+    """The widest supported block (l = 128, k = 100): every kernel at its largest tile
+    shape (gemm_nn NI = 16, gemm_tn MI = 1 x NBL = 16, Jacobi on 128 columns)."""
+    rng = np.random.default_rng(128)
+    m, n, r = 12_000, 1_500, 160
+    u, _ = np.linalg.qr(rng.standard_normal((m, r)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    sig = np.exp(-np.arange(r) / 30.0)
+    a = (u * sig) @ v.T + 1e-9 * rng.standard_normal((m, n)) / np.sqrt(n)
+    om = rng.standard_normal((n, 128))
+    gpu = lowrank_gpu(a, om, 2, 100)
+    ref = oracle.lowrank_svd(a, om, 2, 100)
+    assert gpu[1].size == ref[1].size == 100
+    assert np.max(np.abs(gpu[1] - ref[1])) <= 1e-10 * ref[1][0]
+    assert oracle.ortho_error(gpu[0]) <= 1e-13 and oracle.ortho_error(gpu[2]) <= 1e-13
+    x0 = synth.power_start(n, 5)
+    eg = oracle.spectral_error(a, *gpu, x0)
+    er = oracle.spectral_error(a, *ref, x0)
+    assert abs(eg - er) <= 0.01 * er
