@@ -214,19 +214,27 @@ __global__ void __launch_bounds__(256) k_svd_out(const double* cols, int ldc, in
 
 // M2 (nc x r2 row-major padded): M2[idx_b][a] = sum_c W(b, idx2_c) / (sig[idx_b] T[idx2_c]) Ps(c, a)
 // so that Y~[:, :nc] M2 = Q~_keep T^-1 P = Q P = U.
-__global__ void k_build_m2(const double* W, int r, const int* idx, const double* sig,
-                           const double* T, const int* idx2, int r2, const double* Ps, double* M2,
-                           int ldm) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= r * r2) return;
-  const int b = e / r2, a = e % r2;
-  const int ib = idx[b];
-  double s = 0.0;
-  for (int c = 0; c < r2; ++c) {
+__global__ void __launch_bounds__(256) k_build_m2(const double* W, int r, const int* idx, const double* sig,
+                                                   const double* T, const int* idx2, int r2, const double* Ps,
+                                                   double* M2, int ldm) {
+  // one CTA per row b: wrow[c] = W(b, idx2_c) / T[idx2_c] staged once, then thread a
+  // forms sum_c wrow[c] Ps(c, a) in a fixed order
+  __shared__ double wrow[256];
+  const int b = blockIdx.x;
+  for (int c = threadIdx.x; c < r2; c += blockDim.x) {
     const int c2 = idx2[c];
-    s = fma(W[(size_t)c2 * r + b] / T[c2], Ps[(size_t)a * r2 + c], s);
+    wrow[c] = W[(size_t)c2 * r + b] / T[c2];
   }
-  M2[(size_t)ib * ldm + a] = s / sig[ib];
+  __syncthreads();
+  const int ib = idx[b];
+  const double inv = 1.0 / sig[ib];
+  for (int a = threadIdx.x; a < r2; a += blockDim.x) {
+    const double* pa = Ps + (size_t)a * r2;
+    double s = 0.0;
+#pragma unroll 8
+    for (int c = 0; c < r2; ++c) s = fma(wrow[c], pa[c], s);
+    M2[(size_t)ib * ldm + a] = s * inv;
+  }
 }
 
 // Low-rank final step: flip (V_A[:, a], Ut(:, a)) so V_A's largest entry is positive (R5),
@@ -326,7 +334,7 @@ void svd_out(const double* cols, int ldc, int r2, int r, const double* vals, con
 }
 void build_m2(const double* W, int r, const int* idx, const double* sig, const double* T,
               const int* idx2, int r2, const double* Ps, double* M2, int ldm, cudaStream_t s) {
-  k_build_m2<<<nb((int64_t)r * r2), 256, 0, s>>>(W, r, idx, sig, T, idx2, r2, Ps, M2, ldm);
+  if (r > 0 && r2 > 0) k_build_m2<<<r, 256, 0, s>>>(W, r, idx, sig, T, idx2, r2, Ps, M2, ldm);
 }
 void canon_lowrank(double* VA, int64_t ldva, int n, double* Ut, int ldut, int r3, int r4,
                    cudaStream_t s) {
