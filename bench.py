@@ -92,6 +92,35 @@ class Clocks:
                 "reasons": reasons, "samples": len(rows)}
 
 
+PASS_KERNEL = {"xv": "gemm_nn_kernel", "qnorm": "gemm_nn_kernel", "uout": "gemm_nn_kernel",
+               "alpha": "gemm_nn_kernel", "gram_x": "syrk_kernel", "gram_y": "syrk_kernel",
+               "beta": "gemm_tn_kernel"}
+
+
+def ncu_traffic(config, kind):
+    """DRAM bytes per launch (read + write) of the dominant pass's kernel, from the committed
+    ncu --set full capture of this workload (profiles/r01_<config>_ncu_full_summary.txt, first
+    matching launch in step order), or None when no capture of this workload exists."""
+    path = os.path.join(ROOT, "profiles", f"r01_{config}_ncu_full_summary.txt")
+    name = PASS_KERNEL.get(kind)
+    if not name or not os.path.exists(path):
+        return None
+    order = ["gram_x", "xv", "gram_y", "qnorm", "uout"]  # launch order of one tssvd call
+    want = [k for k in order if PASS_KERNEL.get(k) == name].index(kind) if kind in order else 0
+    seen = 0
+    for line in open(path):
+        if line.startswith(name):
+            if seen == want:
+                try:
+                    rd = float(line.split("dram_rd=")[1].split("G")[0])
+                    wr = float(line.split("dram_wr=")[1].split("G")[0])
+                    return {"bytes_per_launch": round((rd + wr) * 1e9), "source": os.path.relpath(path, ROOT)}
+                except (IndexError, ValueError):
+                    return None
+            seen += 1
+    return None
+
+
 def a_passes(cfg):
     return 2 if cfg["kind"] == "tssvd" else 2 * cfg["iters"] + 2
 
@@ -194,6 +223,7 @@ def run_ours(args, rank, world, local_rank):
     _lib.set_pass_timing(True)
     pass_ms = {}
     pass_flops = {}
+    pass_kinds, pass_bytes = [], []
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
@@ -203,6 +233,8 @@ def run_ours(args, rank, world, local_rank):
         for p in _lib.last_stats()["passes"]:
             pass_ms.setdefault(p["kind"], []).append(p["ms"])
             pass_flops.setdefault(p["kind"], []).append(p["flops"])
+            pass_kinds.append(p["kind"])
+            pass_bytes.append(p["bytes"])
     e1.record(stream)
     barrier()
     _lib.set_pass_timing(False)
@@ -245,7 +277,10 @@ def run_ours(args, rank, world, local_rank):
     achieved = flops / (avg_ms * 1e-3) / 1e12
     roof = {"kernel": dom, "bound": "tensor", "achieved": round(achieved, 3),
             "peak": MEASURED_FP64_DMMA_TFLOPS, "unit": "TFLOP/s",
-            "frac": round(achieved / MEASURED_FP64_DMMA_TFLOPS, 4), "traffic": None,
+            "frac": round(achieved / MEASURED_FP64_DMMA_TFLOPS, 4),
+            "traffic": ncu_traffic(args.config, dom),
+            "algorithmic_bytes_per_launch": round(statistics.mean(
+                [b for k, b in zip(pass_kinds, pass_bytes) if k == dom])) if pass_bytes else None,
             "peak_source": "FP64 DMMA.8x8x4 throughput measured on this pool's B200 by "
                            "tools/fp64_peak.cu (MEASURED_PEAKS.json has no FP64 entry)",
             "share_of_step": round(shares[dom] / t, 4),
