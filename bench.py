@@ -98,13 +98,13 @@ PASS_KERNEL = {"xv": "gemm_nn_kernel", "qnorm": "gemm_nn_kernel", "uout": "gemm_
 
 
 def ncu_traffic(config, kind):
-    """DRAM bytes per launch (read + write) of the dominant pass's kernel, from the committed
-    ncu --set full capture of this workload (profiles/r01_<config>_ncu_full_summary.txt, first
-    matching launch in step order), or None when no capture of this workload exists."""
+    """(DRAM bytes per launch (read + write), source file) of the dominant pass's kernel, from
+    the committed ncu --set full capture of this workload (profiles/r01_<config>_ncu_full_summary.txt,
+    first matching launch in step order), or (None, None) when no capture of this workload exists."""
     path = os.path.join(ROOT, "profiles", f"r01_{config}_ncu_full_summary.txt")
     name = PASS_KERNEL.get(kind)
     if not name or not os.path.exists(path):
-        return None
+        return None, None
     order = ["gram_x", "xv", "gram_y", "qnorm", "uout"]  # launch order of one tssvd call
     want = [k for k in order if PASS_KERNEL.get(k) == name].index(kind) if kind in order else 0
     seen = 0
@@ -114,11 +114,11 @@ def ncu_traffic(config, kind):
                 try:
                     rd = float(line.split("dram_rd=")[1].split("G")[0])
                     wr = float(line.split("dram_wr=")[1].split("G")[0])
-                    return {"bytes_per_launch": round((rd + wr) * 1e9), "source": os.path.relpath(path, ROOT)}
+                    return round((rd + wr) * 1e9), os.path.relpath(path, ROOT)
                 except (IndexError, ValueError):
-                    return None
+                    return None, None
             seen += 1
-    return None
+    return None, None
 
 
 def a_passes(cfg):
@@ -275,10 +275,11 @@ def run_ours(args, rank, world, local_rank):
     avg_ms = statistics.mean(pass_ms[dom])
     flops = statistics.mean(pass_flops[dom])
     achieved = flops / (avg_ms * 1e-3) / 1e12
+    traffic, traffic_src = ncu_traffic(args.config, dom)
     roof = {"kernel": dom, "bound": "tensor", "achieved": round(achieved, 3),
             "peak": MEASURED_FP64_DMMA_TFLOPS, "unit": "TFLOP/s",
             "frac": round(achieved / MEASURED_FP64_DMMA_TFLOPS, 4),
-            "traffic": ncu_traffic(args.config, dom),
+            "traffic": traffic, "traffic_source": traffic_src,
             "algorithmic_bytes_per_launch": round(statistics.mean(
                 [b for k, b in zip(pass_kinds, pass_bytes) if k == dom])) if pass_bytes else None,
             "peak_source": "FP64 DMMA.8x8x4 throughput measured on this pool's B200 by "

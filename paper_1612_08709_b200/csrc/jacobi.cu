@@ -135,7 +135,58 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
   return y;
 }
 
-template <int C, int G, int V>
+// Rotation of the pair (p, q) with Gram entries [[al, ga], [ga, be]], or false
+// when the pair is already orthogonal to tolerance (|ga| <= tol sqrt(al be)) or
+// both columns are negligible.  With d = be - al:
+//   t = tan(theta) = sign(d) 2ga / (|d| + sqrt(d^2 + 4ga^2)),  c = 1/sqrt(1+t^2), s = c t;
+// then x_p' = c x_p - s x_q, x_q' = s x_p + c x_q.  d and 2ga are first scaled by
+// a power of two (exact) so the squares cannot over/underflow; reciprocal and
+// rsqrt by MUFU + two Newton steps (~1 ulp).
+__device__ __forceinline__ bool jac_rot(double al, double be, double ga, double tol2, double skip2,
+                                        double& c, double& sn) {
+  if (!(ga != 0.0 && ga * ga > tol2 * al * be && fmax(al, be) > skip2)) return false;
+  double d = be - al, g2 = ga + ga;
+  const double big = fmax(fabs(d), fabs(g2));
+  const int ex = (int)((__double_as_longlong(big) >> 52) & 0x7ff);        // biased exponent
+  const double sc = __longlong_as_double((long long)(2046 - ex) << 52);  // 2^(1023 - ex)
+  d *= sc;
+  g2 *= sc;
+  const double w = fma(d, d, g2 * g2);
+  const double root = w * rsqrt_nr(w);
+  const double t = (d >= 0.0 ? g2 : -g2) * rcp_nr(fabs(d) + root);
+  c = rsqrt_nr(fma(t, t, 1.0));
+  sn = c * t;
+  return true;
+}
+
+// Dot products (x.x, y.y, x.y) over this lane's first `elim` double2 rows,
+// reduced over an 8-lane group by an xor butterfly (identical in every lane).
+template <int V>
+__device__ __forceinline__ void dots8(const double2 (&x)[V], const double2 (&y)[V], int elim, double& xx,
+                                      double& yy, double& xy) {
+  double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0, c0 = 0.0, c1 = 0.0;
+#pragma unroll
+  for (int e = 0; e < V; ++e)
+    if (e < elim) {
+      a0 = fma(x[e].x, x[e].x, a0);
+      a1 = fma(x[e].y, x[e].y, a1);
+      b0 = fma(y[e].x, y[e].x, b0);
+      b1 = fma(y[e].y, y[e].y, b1);
+      c0 = fma(x[e].x, y[e].x, c0);
+      c1 = fma(x[e].y, y[e].y, c1);
+    }
+  xx = a0 + a1;
+  yy = b0 + b1;
+  xy = c0 + c1;
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) {
+    xx += __shfl_xor_sync(0xffffffffu, xx, o);
+    yy += __shfl_xor_sync(0xffffffffu, yy, o);
+    xy += __shfl_xor_sync(0xffffffffu, xy, o);
+  }
+}
+
+template <int C, int G, int V, bool BLK>
 __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
   Cl<C> cl;
   const int h = cl.rank();
@@ -442,7 +493,111 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
   const long long t_chol = clock64();
   int sweep = 0, rounds = 0;
   bool converged = K <= 1;
-  {
+  if (BLK && C == 1 && K > 64 && K <= 8 * JW) {
+    // Warp-block ordering (one CTA).  The K columns are taken four at a time
+    // ("blocks", padded to an even number of blocks with the zero slot).  In a
+    // block round warp w holds the block pair (T, B) that the circle ordering
+    // over blocks assigns it, one column of each per 8-lane group, and rotates
+    // the 16 cross pairs (T_g, B_(g+s) mod 4) in four sub-rounds; between
+    // sub-rounds the B columns move one group over by a lane shuffle.  The six
+    // pairs inside every block are rotated at the first block round of a sweep
+    // (three sub-rounds, partner group g xor m).  Every pair is rotated once per
+    // sweep (a cyclic ordering, as in the element ordering below), but shared
+    // memory is touched only to load and store eight columns per block round,
+    // and the CTA synchronises once per block round instead of once per round.
+    // Measured on B200 (tools/jac_bench.py): 2x faster than the element
+    // ordering at K = 106, ~10% at K = 82, no gain below K ~ 64 (the four
+    // sub-rounds' dependency chains, not shared memory, then bound a round).
+    static_assert(!BLK || G == 8, "warp-block sweeps use 8-lane groups");
+    const int NB = (K + 3) / 4, NBE = NB + (NB & 1), W = NBE / 2;
+    for (int k = K + tid; k < 4 * NBE; k += JT) s_order[k] = nslots;
+    __syncthreads();
+    const int g = lane >> 3, gl = lane & 7;
+    const int dloc = min(nloc, a.dpad);
+    const int elim = dloc > 2 * gl ? (dloc - 2 * gl + 15) / 16 : 0;
+    // the six pairs of the block held in x (group g holds its column g)
+    auto inner = [&](double2 (&x)[V]) -> int {
+      int r = 0;
+#pragma unroll 1
+      for (int m = 1; m < 4; ++m) {
+        double2 y[V];
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          y[e].x = __shfl_xor_sync(0xffffffffu, x[e].x, 8 * m);
+          y[e].y = __shfl_xor_sync(0xffffffffu, x[e].y, 8 * m);
+        }
+        // pair (p, q) = (lower group, higher group): both groups compute the same sums
+        const bool lo = g < (g ^ m);
+        double xx, yy, xy, c, sn;
+        dots8<V>(x, y, elim, xx, yy, xy);
+        if (jac_rot(lo ? xx : yy, lo ? yy : xx, xy, tol2, skip2, c, sn)) {
+          const double sa = lo ? -sn : sn;  // x_p' = c x_p - s x_q,  x_q' = s x_p + c x_q
+#pragma unroll
+          for (int e = 0; e < V; ++e)
+            x[e] = make_double2(fma(c, x[e].x, sa * y[e].x), fma(c, x[e].y, sa * y[e].y));
+          r = 1;
+        }
+      }
+      return r;
+    };
+    for (; sweep < a.max_sweeps && !converged; ++sweep) {
+      int any = 0;
+      for (int br = 0; br < NBE - 1; ++br, ++rounds) {
+        int rot = 0;
+        if (warp < W) {
+          const int pT = warp ? 1 + (warp - 1 + br) % (NBE - 1) : 0;
+          const int pB = 1 + (NBE - 2 - warp + br) % (NBE - 1);
+          if (br == 0) {  // the six pairs inside each of the two blocks
+#pragma unroll 1
+            for (int hb = 0; hb < 2; ++hb) {
+              double2* xc = reinterpret_cast<double2*>(X + s_order[4 * (hb ? pB : pT) + g] * P) + gl;
+              double2 x[V];
+#pragma unroll
+              for (int e = 0; e < V; ++e) x[e] = xc[8 * e];
+              if (inner(x)) {
+#pragma unroll
+                for (int e = 0; e < V; ++e) xc[8 * e] = x[e];
+                rot = 1;
+              }
+            }
+            __syncwarp();
+          }
+          double2* xt = reinterpret_cast<double2*>(X + s_order[4 * pT + g] * P) + gl;
+          const double2* xb0 = reinterpret_cast<const double2*>(X + s_order[4 * pB + g] * P) + gl;
+          double2 t[V], b[V];
+#pragma unroll
+          for (int e = 0; e < V; ++e) t[e] = xt[8 * e], b[e] = xb0[8 * e];
+#pragma unroll 1
+          for (int sr = 0; sr < 4; ++sr) {
+            if (sr) {  // group g takes group g+1's B column
+              const int src = (lane + 8) & 31;
+#pragma unroll
+              for (int e = 0; e < V; ++e) {
+                b[e].x = __shfl_sync(0xffffffffu, b[e].x, src);
+                b[e].y = __shfl_sync(0xffffffffu, b[e].y, src);
+              }
+            }
+            double al, be, ga, c, sn;
+            dots8<V>(t, b, elim, al, be, ga);
+            if (jac_rot(al, be, ga, tol2, skip2, c, sn)) {
+#pragma unroll
+              for (int e = 0; e < V; ++e) {
+                const double2 tp = t[e], bq = b[e];
+                t[e] = make_double2(fma(c, tp.x, -sn * bq.x), fma(c, tp.y, -sn * bq.y));
+                b[e] = make_double2(fma(sn, tp.x, c * bq.x), fma(sn, tp.y, c * bq.y));
+              }
+              rot = 1;
+            }
+          }
+          double2* xb = reinterpret_cast<double2*>(X + s_order[4 * pB + ((g + 3) & 3)] * P) + gl;
+#pragma unroll
+          for (int e = 0; e < V; ++e) xt[8 * e] = t[e], xb[8 * e] = b[e];
+        }
+        any |= __syncthreads_or(rot);
+      }
+      converged = !any;
+    }
+  } else {
   // Circle (round-robin) ordering on positions 0..NE-1: in round r, pair i is
   // (p, q) = (i ? 1 + (i-1+r) mod (NE-1) : 0, 1 + (NE-2-i+r) mod (NE-1)),
   // advanced incrementally.  An odd K is padded with the all-zero slot
@@ -521,22 +676,8 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
         al = be = ga = 0.0;
         for (int qc = 0; qc < C; ++qc) al += xb[qc * 4], be += xb[qc * 4 + 1], ga += xb[qc * 4 + 2];
       }
-      if (has && ga != 0.0 && ga * ga > tol2 * al * be && fmax(al, be) > skip2) {
-        // rotation zeroing the (p, q) entry of [[al, ga], [ga, be]], d = be - al:
-        //   t = tan(theta) = sign(d) 2ga / (|d| + sqrt(d^2 + 4ga^2)),  c = 1/sqrt(1+t^2), s = c t.
-        // d and 2ga are first scaled by a power of two (exact) so the squares cannot
-        // over/underflow; reciprocal / rsqrt by MUFU + two Newton steps (~1 ulp).
-        double d = be - al, g2 = ga + ga;
-        const double big = fmax(fabs(d), fabs(g2));
-        const int ex = (int)((__double_as_longlong(big) >> 52) & 0x7ff);  // biased exponent
-        const double sc = __longlong_as_double((long long)(2046 - ex) << 52);  // 2^(1023 - ex + 0)
-        d *= sc;
-        g2 *= sc;
-        const double w = fma(d, d, g2 * g2);
-        const double root = w * rsqrt_nr(w);
-        const double t = (d >= 0.0 ? g2 : -g2) * rcp_nr(fabs(d) + root);
-        const double c = rsqrt_nr(fma(t, t, 1.0));
-        const double sn = c * t;
+      double c, sn;
+      if (has && jac_rot(al, be, ga, tol2, skip2, c, sn)) {
 #pragma unroll
         for (int e = 0; e < V; ++e) {
           xp[G * e] = make_double2(fma(c, vp[e].x, -sn * vq[e].x), fma(c, vp[e].y, -sn * vq[e].y));
@@ -551,9 +692,7 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
     }
     converged = !any;
   }
-
   }
-
   const long long t_sweeps = clock64();
   // ------------------------------------------ norms, order, write back ----
   col_norms(K);
@@ -600,9 +739,9 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
 }
 
 // ------------------------------------------------------------- launch ----
-template <int C, int G, int V>
+template <int C, int G, int V, bool BLK>
 static cudaError_t jac_go(const JacArgs& a, size_t smem, cudaStream_t s) {
-  auto kern = jacobi_kernel<C, G, V>;
+  auto kern = jacobi_kernel<C, G, V, BLK>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -620,16 +759,16 @@ static cudaError_t jac_go(const JacArgs& a, size_t smem, cudaStream_t s) {
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-template <int C, int G>
+template <int C, int G, bool BLK = false>
 static cudaError_t jac_v(const JacArgs& a, size_t smem, cudaStream_t s) {
   switch (a.V) {
-    case 2: return jac_go<C, G, 2>(a, smem, s);
-    case 3: return jac_go<C, G, 3>(a, smem, s);
-    case 4: return jac_go<C, G, 4>(a, smem, s);
-    case 5: return jac_go<C, G, 5>(a, smem, s);
-    case 6: return jac_go<C, G, 6>(a, smem, s);
-    case 7: return jac_go<C, G, 7>(a, smem, s);
-    default: return jac_go<C, G, 8>(a, smem, s);
+    case 2: return jac_go<C, G, 2, BLK>(a, smem, s);
+    case 3: return jac_go<C, G, 3, BLK>(a, smem, s);
+    case 4: return jac_go<C, G, 4, BLK>(a, smem, s);
+    case 5: return jac_go<C, G, 5, BLK>(a, smem, s);
+    case 6: return jac_go<C, G, 6, BLK>(a, smem, s);
+    case 7: return jac_go<C, G, 7, BLK>(a, smem, s);
+    default: return jac_go<C, G, 8, BLK>(a, smem, s);
   }
 }
 
@@ -688,6 +827,19 @@ static cudaError_t jac_dispatch(JacArgs a, cudaStream_t s) {
       if (jac_smem(C, nslots, 2 * G * V) > budget) continue;
       const double cost = jac_round_cost(C, G, V, npairs);
       if (cost < best) best = cost, bC = C, bG = G, bV = V, bLh = Lh;
+    }
+  }
+  // warp-block sweeps (one CTA, 8-lane groups) when more than 64 columns may
+  // survive the Cholesky, they fit one pass of the 16 warps and one CTA holds
+  // them (TSSVD_JAC_BLK=0 disables; K <= 64 falls back to the element ordering)
+  static const bool blk_ok = !getenv("TSSVD_JAC_BLK") || atoi(getenv("TSSVD_JAC_BLK")) != 0;
+  if (blk_ok && !force_g && force_c <= 1 && nslots > 64 && nslots <= 8 * JW) {
+    const int V = std::max(2, (int)ceil_div(a.L, 16));
+    if (V <= 8 && jac_smem(1, nslots, 16 * V) <= budget) {
+      a.Lh = (a.L + 1) & ~1;
+      a.V = V;
+      a.P = 16 * V;
+      return jac_v<1, 8, true>(a, jac_smem(1, nslots, a.P), s);
     }
   }
   if (!bC) return cudaErrorInvalidValue;
