@@ -36,7 +36,7 @@ size_t gemm_nn_m_doubles(int k, int c);  // size of the padded M buffer
 // Z (n x l, ld ldz) partials: Zp[split][n_pad x ldz] = X[rows, :n]^T * Y[rows, :l]
 // reduced over `splits` row ranges.
 struct TnPlan {
-  int cb, mi, nbl, colblocks, splits, kr, nst, ldz;
+  int cb, mi, nbl, xr, colblocks, splits, kr, nst, ldz;  // xr: remainder columns on the FMA pipe
   int64_t rows_per_split;
   size_t part_doubles;
 };

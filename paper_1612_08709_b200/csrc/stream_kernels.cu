@@ -326,9 +326,15 @@ cudaError_t launch_reduce_parts(const double* part, int np, int64_t stride, int6
 // streamed in chunks of KC (= 4 mod 8) columns: a stage holds the box
 // X[tile rows, k0:k0+KC] and the box M[k0:k0+KC, :] (M row-major,
 // ld = smem_ld(c)); columns >= k of X and rows >= k of M arrive as zeros.
+// XR > 0 (c = 8 NIW + XR, WC = 1): the last XR columns go to the FP64 FMA pipe
+// instead of a DMMA tile that would be (8 - XR)/8 zeros: lane (g, t) already
+// holds X[row g][4 kk + t] as its DMMA A fragment, multiplies it by the
+// broadcast M[4 kk + t][8 NIW + x] and the four t-partials are summed by an xor
+// butterfly at the end of the tile (c = 25 = 3*8 + 1: 25 instead of 32 columns
+// of FP64 work).
 static constexpr int NN_CW = 8;  // consumer warps
 
-template <int MI, int NIW, int WC>
+template <int MI, int NIW, int WC, int XR>
 __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
     const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tm, int64_t m, int k,
     int KC, int kc_count, int LDM, int c, double* Y, int64_t ldy, double* __restrict__ norm_part,
@@ -336,7 +342,9 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int RW = NN_CW / WC;
   constexpr int R = 8 * MI * RW;
-  constexpr int CP = NIW * WC * 8;  // padded output columns
+  static_assert(XR == 0 || WC == 1, "remainder columns need a single column group");
+  constexpr int NB = NIW + (XR > 0);  // column blocks per warp in the norm layout
+  constexpr int CP = NB * WC * 8;     // padded output columns (norm_part stride)
   const Ring ring{reinterpret_cast<uint64_t*>(smem)};
   double* buf = reinterpret_cast<double*>(smem + kBarBytes);
   const int xs_d = R * KC, stage_d = xs_d + KC * LDM;
@@ -371,13 +379,20 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
     for (int j = 0; j < NIW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   // per-warp column sums of squares (norm epilogue): in registers over the whole
   // run when they fit (NRM), else per tile into a shared-memory row after the stages
-  constexpr bool NRM = 2 * MI * NIW + 2 * NIW <= 56;  // (measured: no spills up to 56)
+  constexpr bool NRM = 2 * MI * NIW + 2 * NIW + MI * XR + XR <= 56;  // (measured: no spills up to 56)
   double nacc[NRM ? NIW : 1][2];
 #pragma unroll
   for (int j = 0; j < (NRM ? NIW : 1); ++j) nacc[j][0] = nacc[j][1] = 0.0;
-  double* red = buf + nst * stage_d + warp * NIW * 8;
+  double ex[MI][XR > 0 ? XR : 1], nx[XR > 0 ? XR : 1];  // remainder-column partials and norms
+#pragma unroll
+  for (int x = 0; x < (XR > 0 ? XR : 1); ++x) {
+    nx[x] = 0.0;
+#pragma unroll
+    for (int i = 0; i < MI; ++i) ex[i][x] = 0.0;
+  }
+  double* red = buf + nst * stage_d + warp * NB * 8;
   if (norm_part && !NRM)
-    for (int col = lane; col < NIW * 8; col += 32) red[col] = 0.0;
+    for (int col = lane; col < NB * 8; col += 32) red[col] = 0.0;
 
   for (int64_t s = 0; s < nsteps; ++s) {
     const int b = (int)(s % nst);
@@ -386,6 +401,8 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
     const double* ms = buf + b * stage_d + xs_d + t * LDM + col0 + g;
     const int kc_here = (int)(s % kc_count);
     const int nks = min(KC / 4, (k - kc_here * KC + 3) / 4);  // k-steps holding real columns
+    // (software-pipelining the fragment loads, as gemm_tn does, measured slower
+    // here: 7.9 -> 9.0 ms per c3 alpha pass)
     for (int kk = 0; kk < nks; ++kk) {
       double a[MI];
 #pragma unroll
@@ -395,6 +412,14 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
         const double bf = ms[kk * 4 * LDM + j * 8];
 #pragma unroll
         for (int i = 0; i < MI; ++i) dmma(acc[i][j], a[i], bf);
+      }
+      if constexpr (XR > 0) {  // M[4kk + t][8 NIW + x]: one broadcast load per t
+#pragma unroll
+        for (int x = 0; x < XR; ++x) {
+          const double mv = ms[kk * 4 * LDM - g + NIW * 8 + x];
+#pragma unroll
+          for (int i = 0; i < MI; ++i) ex[i][x] = fma(a[i], mv, ex[i][x]);
+        }
       }
     }
     __syncwarp();
@@ -422,6 +447,21 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
             v += __shfl_xor_sync(0xffffffffu, v, 16);
             if (g == 0) red[j * 8 + 2 * t + e] += v;
           }
+      }
+      if constexpr (XR > 0) {  // remainder columns: sum the four t-partials, store, norms
+#pragma unroll
+        for (int i = 0; i < MI; ++i) {
+          const int64_t row = tile * R + (rg * MI + i) * 8 + g;
+#pragma unroll
+          for (int x = 0; x < XR; ++x) {
+            double v = ex[i][x];
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            v += __shfl_xor_sync(0xffffffffu, v, 2);
+            ex[i][x] = 0.0;
+            if (t == x && row < m && Y) Y[row * ldy + NIW * 8 + x] = v;
+            nx[x] = fma(v, v, nx[x]);  // rows beyond m are zero
+          }
+        }
       }
 #pragma unroll
       for (int i = 0; i < MI; ++i) {
@@ -455,26 +495,42 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
           if (g == 0) red[j * 8 + 2 * t + e] = v;
         }
     }
+    if constexpr (XR > 0) {  // every t-lane holds the same sums: sum over g only
+#pragma unroll
+      for (int x = 0; x < XR; ++x) {
+        double v = nx[x];
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        nx[x] = v;
+      }
+      if (lane < 8) red[NIW * 8 + lane] = lane == 0 ? nx[0] : (XR > 1 && lane == 1 ? nx[XR > 1 ? 1 : 0] : 0.0);
+    }
     bar_consumers(NN_CW * 32);
     const double* red0 = buf + nst * stage_d;
     for (int col = threadIdx.x; col < CP; col += NN_CW * 32) {
-      const int cgi = col / (NIW * 8), cc = col % (NIW * 8);
+      const int cgi = col / (NB * 8), cc = col % (NB * 8);
       double v = 0.0;
-      for (int r2 = 0; r2 < RW; ++r2) v += red0[(cgi * RW + r2) * NIW * 8 + cc];
+      for (int r2 = 0; r2 < RW; ++r2) v += red0[(cgi * RW + r2) * NB * 8 + cc];
       norm_part[(size_t)blockIdx.x * CP + col] = v;
     }
   }
 }
 
 // Warp grid and rows per tile from the accumulator budget (<= 24 8x8 tiles,
-// <= 16 column blocks per warp).
+// <= 16 column blocks per warp); c = 8 ni + 1 or + 2 (1 <= ni <= 4, where the
+// extra accumulators still fit without spills) puts the last one or two columns
+// on the FMA pipe (xr).
 struct NnShape {
-  int wc, niw, mi;
+  int ni, xr, wc, niw, mi;
 };
-static NnShape nn_shape(int ni) {
+static int nn_xr(int c) { return (c % 8 == 1 || c % 8 == 2) && c > 8 && c / 8 <= 4 ? c % 8 : 0; }
+static NnShape nn_shape(int c) {
   NnShape sh;
-  sh.wc = ni <= 16 ? 1 : 2;
-  sh.niw = (ni + sh.wc - 1) / sh.wc;
+  sh.xr = nn_xr(c);
+  sh.ni = sh.xr ? c / 8 : (c + 7) / 8;
+  sh.wc = sh.ni <= 16 ? 1 : 2;
+  sh.niw = (sh.ni + sh.wc - 1) / sh.wc;
   sh.mi = std::max(1, std::min(4, 24 / sh.niw));
   return sh;
 }
@@ -490,11 +546,11 @@ struct NnPlan {
 // preferred).  (Measured at c2: 2 chunks x 2 stages beat 4 chunks x 4 stages.)
 static NnPlan plan_nn(int64_t m, int k, int c) {
   NnPlan p;
-  p.ni = (c + 7) / 8;
-  p.sh = nn_shape(p.ni);
+  p.sh = nn_shape(c);
+  p.ni = p.sh.ni;
   p.R = 8 * p.sh.mi * (NN_CW / p.sh.wc);
   p.ldm = std::min(smem_ld(c), 256);  // smem row stride of the M box (TMA box limit)
-  const size_t red = (size_t)NN_CW * p.sh.niw * 8 * 8;
+  const size_t red = (size_t)NN_CW * (p.sh.niw + (p.sh.xr > 0)) * 8 * 8;
   const size_t budget = dev_info().smem_optin - kBarBytes - red;
   double best = 1e300;
   p.KC = 28;
@@ -518,20 +574,20 @@ static NnPlan plan_nn(int64_t m, int k, int c) {
 }
 
 int gemm_nn_grid(int64_t m, int c) {
-  const NnShape sh = nn_shape((c + 7) / 8);
+  const NnShape sh = nn_shape(c);
   const int R = 8 * sh.mi * (NN_CW / sh.wc);
   return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, R), dev_info().sms));
 }
 int gemm_nn_part_stride(int c) {
-  const NnShape sh = nn_shape((c + 7) / 8);
-  return sh.niw * sh.wc * 8;
+  const NnShape sh = nn_shape(c);
+  return (sh.niw + (sh.xr > 0)) * sh.wc * 8;
 }
 size_t gemm_nn_m_doubles(int k, int c) { return (size_t)ceil_div(k + 1, 32) * 32 * smem_ld(c); }
 
-template <int MI, int NIW, int WC>
+template <int MI, int NIW, int WC, int XR>
 static cudaError_t nn_go(const NnPlan& p, const CUtensorMap& tx, const CUtensorMap& tm, int64_t m,
                          int k, int c, double* Y, int64_t ldy, double* norm_part, cudaStream_t s) {
-  auto kern = gemm_nn_kernel<MI, NIW, WC>;
+  auto kern = gemm_nn_kernel<MI, NIW, WC, XR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
   if (e != cudaSuccess) return e;
   kern<<<p.grid, (NN_CW + 1) * 32, p.smem, s>>>(tx, tm, m, k, p.KC, p.kcc, p.ldm, c, Y, ldy, norm_part,
@@ -539,13 +595,13 @@ static cudaError_t nn_go(const NnPlan& p, const CUtensorMap& tx, const CUtensorM
   return cudaGetLastError();
 }
 
-template <int NI>
+template <int NI, int XR = 0>
 static cudaError_t nn_ni_go(const NnPlan& p, const CUtensorMap& tx, const CUtensorMap& tm, int64_t m,
                             int k, int c, double* Y, int64_t ldy, double* np, cudaStream_t s) {
   constexpr int WC = NI <= 16 ? 1 : 2;
   constexpr int NIW = (NI + WC - 1) / WC;
   constexpr int MI = 24 / NIW < 1 ? 1 : (24 / NIW > 4 ? 4 : 24 / NIW);
-  return nn_go<MI, NIW, WC>(p, tx, tm, m, k, c, Y, ldy, np, s);
+  return nn_go<MI, NIW, WC, XR>(p, tx, tm, m, k, c, Y, ldy, np, s);
 }
 
 cudaError_t launch_gemm_nn(const double* X, int64_t ldx, int64_t m, int k, const double* M,
@@ -562,6 +618,14 @@ cudaError_t launch_gemm_nn(const double* X, int64_t ldx, int64_t m, int k, const
   if (e != cudaSuccess) return e;
   e = make_tmap(&tm, M, k, smem_ld(c), smem_ld(c), p.KC, p.ldm);
   if (e != cudaSuccess) return e;
+#define NN_XCASE(N) \
+  case N: return p.sh.xr == 1 ? nn_ni_go<N, 1>(p, tx, tm, m, k, c, Y, ldy, norm_part, s) \
+                              : nn_ni_go<N, 2>(p, tx, tm, m, k, c, Y, ldy, norm_part, s);
+  if (p.sh.xr) switch (p.ni) {
+      NN_XCASE(1) NN_XCASE(2) NN_XCASE(3) NN_XCASE(4)
+      default: return cudaErrorInvalidValue;
+    }
+#undef NN_XCASE
 #define NN_CASE(N) \
   case N: return nn_ni_go<N>(p, tx, tm, m, k, c, Y, ldy, norm_part, s);
   switch (p.ni) {
@@ -582,9 +646,12 @@ cudaError_t launch_gemm_nn(const double* X, int64_t ldx, int64_t m, int k, const
 // w*MI..w*MI+MI-1 and all NBL column blocks of Y.  Fragments: A = X^T (8x4)
 // -> Xs[k][i0+g], B = Y (4x8) -> Ys[k][j0+g], k = kk*4 + t.  The X box is
 // CB + 4 columns wide (the 4 extra columns only pad the smem rows to = 4 mod 8).
+// XR > 0 (l = 8 NBL + XR): the last XR columns of Y on the FMA pipe, as in gemm_nn
+// (lane (g, t) holds X[4kk + t][i0 + g] as its A fragment; the four t-partials
+// are summed by a butterfly before the store).
 static constexpr int TN_CW = 8;
 
-template <int MI, int NBL>
+template <int MI, int NBL, int XR>
 __global__ void __launch_bounds__(32 * (TN_CW + 1)) gemm_tn_kernel(
     const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap ty, int64_t m, int n,
     int64_t rps, double* __restrict__ part, int ldz, int64_t n_pad, int KR, int nst) {
@@ -621,22 +688,49 @@ __global__ void __launch_bounds__(32 * (TN_CW + 1)) gemm_tn_kernel(
   for (int i = 0; i < MI; ++i)
 #pragma unroll
     for (int j = 0; j < NBL; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  double ex[MI][XR > 0 ? XR : 1];
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int x = 0; x < (XR > 0 ? XR : 1); ++x) ex[i][x] = 0.0;
 
   for (int s = 0; s < nsteps; ++s) {
     const int b = s % nst;
     mbar_wait(ring.full(b), (s / nst) & 1);
     const double* xs = buf + b * stage_d + t * LDXS + warp * MI * 8 + g;
     const double* ys = buf + b * stage_d + xs_d + t * LDYS + g;
-    for (int kk = 0; kk < KR / 4; ++kk) {
-      double a[MI], bf[NBL];
+    // software-pipelined fragment loads, as in gemm_nn
+    constexpr int XRA = XR > 0 ? XR : 1;
+    const int nkk = KR / 4;
+    double a[MI], bf[NBL], yv[XRA];
+    auto load = [&](int q, double (&fa)[MI], double (&fb)[NBL], double (&fy)[XRA]) {
 #pragma unroll
-      for (int i = 0; i < MI; ++i) a[i] = xs[kk * 4 * LDXS + i * 8];
+      for (int i = 0; i < MI; ++i) fa[i] = xs[q * 4 * LDXS + i * 8];
 #pragma unroll
-      for (int j = 0; j < NBL; ++j) bf[j] = ys[kk * 4 * LDYS + j * 8];
+      for (int j = 0; j < NBL; ++j) fb[j] = ys[q * 4 * LDYS + j * 8];
+      if constexpr (XR > 0)  // Y[4q + t][8 NBL + x]: one broadcast load per t
+#pragma unroll
+        for (int x = 0; x < XR; ++x) fy[x] = ys[q * 4 * LDYS + NBL * 8 + x - g];
+    };
+    load(0, a, bf, yv);
+    for (int kk = 0; kk < nkk; ++kk) {
+      double an[MI], bn[NBL], yn[XRA];
+      load(min(kk + 1, nkk - 1), an, bn, yn);
 #pragma unroll
       for (int i = 0; i < MI; ++i)
 #pragma unroll
         for (int j = 0; j < NBL; ++j) dmma(acc[i][j], a[i], bf[j]);
+      if constexpr (XR > 0)
+#pragma unroll
+        for (int x = 0; x < XR; ++x)
+#pragma unroll
+          for (int i = 0; i < MI; ++i) ex[i][x] = fma(a[i], yv[x], ex[i][x]);
+#pragma unroll
+      for (int i = 0; i < MI; ++i) a[i] = an[i];
+#pragma unroll
+      for (int j = 0; j < NBL; ++j) bf[j] = bn[j];
+#pragma unroll
+      for (int x = 0; x < XRA; ++x) yv[x] = yn[x];
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(ring.empty(b));
@@ -652,14 +746,32 @@ __global__ void __launch_bounds__(32 * (TN_CW + 1)) gemm_tn_kernel(
       *reinterpret_cast<double2*>(P + (size_t)row * ldz + j * 8 + 2 * t) =
           make_double2(acc[i][j][0], acc[i][j][1]);
   }
+  if constexpr (XR > 0) {  // columns 8 NBL .. 8 NBL + 7 of the partial: remainder sums, then zeros
+#pragma unroll
+    for (int i = 0; i < MI; ++i) {
+      double v0 = ex[i][0], v1 = 0.0;
+      v0 += __shfl_xor_sync(0xffffffffu, v0, 1);
+      v0 += __shfl_xor_sync(0xffffffffu, v0, 2);
+      if constexpr (XR > 1) {
+        v1 = ex[i][XR > 1 ? 1 : 0];
+        v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
+        v1 += __shfl_xor_sync(0xffffffffu, v1, 2);
+      }
+      const int row = c0 + (warp * MI + i) * 8 + g;
+      if (row < n)
+        *reinterpret_cast<double2*>(P + (size_t)row * ldz + NBL * 8 + 2 * t) =
+            t == 0 ? make_double2(v0, v1) : make_double2(0.0, 0.0);
+    }
+  }
 }
 
 TnPlan plan_gemm_tn(int64_t m, int n, int l) {
   TnPlan p;
-  p.nbl = (l + 7) / 8;
+  p.xr = (l % 8 == 1 || l % 8 == 2) && l > 8 && l / 8 <= 5 ? l % 8 : 0;  // remainder columns on the FMA pipe
+  p.nbl = p.xr ? l / 8 : (l + 7) / 8;
   p.mi = p.nbl <= 8 ? 2 : 1;
   p.cb = 8 * p.mi * TN_CW;
-  p.ldz = p.nbl * 8;
+  p.ldz = pad8(l);
   p.colblocks = (int)ceil_div(n, p.cb);
   const size_t row_bytes = (size_t)((p.cb + 4) + (p.nbl * 8 + 4)) * 8;
   const size_t budget = dev_info().smem_optin - kBarBytes;
@@ -685,16 +797,16 @@ TnPlan plan_gemm_tn(int64_t m, int n, int l) {
   return p;
 }
 
-template <int MI, int NBL>
+template <int MI, int NBL, int XR = 0>
 static cudaError_t tn_go(const TnPlan& p, const CUtensorMap& tx, const CUtensorMap& ty, int64_t m, int n,
                          double* part, cudaStream_t s) {
   const size_t smem = kBarBytes + (size_t)p.nst * p.kr * ((p.cb + 4) + (NBL * 8 + 4)) * 8;
-  cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel<MI, NBL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  auto kern = gemm_tn_kernel<MI, NBL, XR>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid(p.colblocks, p.splits);
-  gemm_tn_kernel<MI, NBL><<<grid, (TN_CW + 1) * 32, smem, s>>>(tx, ty, m, n, p.rows_per_split, part, p.ldz,
-                                                               (int64_t)p.colblocks * p.cb, p.kr, p.nst);
+  kern<<<grid, (TN_CW + 1) * 32, smem, s>>>(tx, ty, m, n, p.rows_per_split, part, p.ldz,
+                                            (int64_t)p.colblocks * p.cb, p.kr, p.nst);
   return cudaGetLastError();
 }
 
@@ -706,6 +818,12 @@ cudaError_t launch_gemm_tn(const TnPlan& p, const double* X, int64_t ldx, int64_
   if (e != cudaSuccess) return e;
   e = make_tmap(&ty, Y, m, l, ldy, p.kr, p.nbl * 8 + 4);
   if (e != cudaSuccess) return e;
+#define TN_XCASE(MI, NB)                                                                   \
+  if (p.xr && p.mi == MI && p.nbl == NB)                                                   \
+    return p.xr == 1 ? tn_go<MI, NB, 1>(p, tx, ty, m, n, part, s) : tn_go<MI, NB, 2>(p, tx, ty, m, n, part, s);
+  TN_XCASE(2, 1) TN_XCASE(2, 2) TN_XCASE(2, 3) TN_XCASE(2, 4) TN_XCASE(2, 5)
+#undef TN_XCASE
+  if (p.xr) return cudaErrorInvalidValue;
 #define TN_CASE(MI, NB) \
   if (p.mi == MI && p.nbl == NB) return tn_go<MI, NB>(p, tx, ty, m, n, part, s);
   TN_CASE(2, 1) TN_CASE(2, 2) TN_CASE(2, 3) TN_CASE(2, 4)

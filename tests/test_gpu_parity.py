@@ -43,8 +43,10 @@ def test_gram_kernel_vs_oracle(m, n):
 
 @pytest.mark.parametrize("m,k,c", [(1, 2, 1), (777, 10, 9), (100_003, 100, 100), (50_001, 200, 200),
                                    (10_000, 100, 55), (3_001, 256, 256), (1000, 20_000, 25),
-                                   (999, 4_000, 60)])
+                                   (999, 4_000, 60), (5_003, 300, 10), (4_097, 50, 17),
+                                   (3_001, 128, 129), (2_001, 64, 130), (1_001, 70, 131)])
 def test_matmul_kernel_vs_numpy(m, k, c):
+    """c = 8j+1 / 8j+2 (j <= 16) run the last columns on the FMA pipe (remainder path)."""
     rng = np.random.default_rng(m + k + c)
     x = rng.standard_normal((m, k + (k & 1)))[:, :k] if k & 1 else rng.standard_normal((m, k))
     mm = rng.standard_normal((k, c))
@@ -69,8 +71,10 @@ def test_matmul_in_place():
 
 
 @pytest.mark.parametrize("m,n,l", [(1, 2, 1), (1000, 512, 25), (20_011, 2_000, 25), (5_000, 4_000, 60),
-                                   (3_000, 1_000, 128), (300, 20_000, 32)])
+                                   (3_000, 1_000, 128), (300, 20_000, 32), (4_001, 700, 9),
+                                   (3_003, 1_500, 26), (2_000, 300, 66), (1_000, 100, 65), (777, 50, 74)])
 def test_matmul_tn_kernel_vs_numpy(m, n, l):
+    """l = 8j+1 / 8j+2 (j <= 8) run the last columns on the FMA pipe (remainder path)."""
     rng = np.random.default_rng(m + n + l)
     x = rng.standard_normal((m, n))
     y = rng.standard_normal((m, l + (l & 1)))
