@@ -110,9 +110,13 @@ __device__ __forceinline__ void ring_init(Ring r, int nst, int consumers) {
 // row block: the fragment of column block c at k-step kk is Xs[kk*4+t][c*8+g]
 // in the A (= X^T) and the B role alike.
 static constexpr int SYRK_KR = 32;
-static constexpr int SYRK_TPW = 8;
+static constexpr int SYRK_TPW = 11;
+// CTAs per SM: runs of <= 6 tiles fit 64 registers (two CTAs per SM), longer
+// runs need up to 128 (one CTA per SM)
+static constexpr int syrk_minb(int tpw) { return tpw <= 6 ? 2 : 1; }
 
-__global__ void __launch_bounds__(512, 2) syrk_kernel(const __grid_constant__ CUtensorMap tx, int64_t m,
+template <int TPW, int MINB>
+__global__ void __launch_bounds__(512, MINB) syrk_kernel(const __grid_constant__ CUtensorMap tx, int64_t m,
                                                       int w, int W, int64_t rpc, double* __restrict__ part,
                                                       int nst, int tps, int tpw) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -145,26 +149,43 @@ __global__ void __launch_bounds__(512, 2) syrk_kernel(const __grid_constant__ CU
   int I0 = 0;
   while ((I0 + 1) * (I0 + 2) / 2 <= q0) ++I0;
   const int J0 = q0 - I0 * (I0 + 1) / 2;
-  double acc[SYRK_TPW][2];
+  // Per tile: the shared-memory offsets of its row and column fragments within a
+  // k-row, packed (row << 16 | col), and a bit when it starts a new block row.
+  // Tiles past the run repeat the last one (computed, never stored), so the
+  // DMMA sequence of a k-step is branch-free: all column fragments are loaded
+  // first, then each DMMA issues behind at most a predicated row-fragment load.
+  uint32_t off[TPW];
+  uint32_t newrow = 0;
+  {
+    int I = I0, J = J0;
 #pragma unroll
-  for (int k = 0; k < SYRK_TPW; ++k) acc[k][0] = acc[k][1] = 0.0;
+    for (int k = 0; k < TPW; ++k) {
+      off[k] = k < nt || k == 0 ? (uint32_t)(I * 8) << 16 | (uint32_t)(J * 8) : off[k > 0 ? k - 1 : 0];
+      if (k > 0 && k < nt && J == 0) newrow |= 1u << k;
+      if (++J > I) ++I, J = 0;
+    }
+  }
+  double acc[TPW][2];
+#pragma unroll
+  for (int k = 0; k < TPW; ++k) acc[k][0] = acc[k][1] = 0.0;
 
   for (int s = 0; s < nsteps; ++s) {
     const int b = s % nst;
     mbar_wait(ring.full(b), (s / nst) & 1);
     const double* base = buf + b * stage_d + t * W + g;
+    if (nt > 0) {
 #pragma unroll
-    for (int kk = 0; kk < SYRK_KR / 4 && nt > 0; ++kk) {
-      const double* rp = base + kk * 4 * W;
-      double fi = rp[I0 * 8];
-      int I = I0, J = J0;
+      for (int kk = 0; kk < SYRK_KR / 4; ++kk) {
+        const double* rp = base + kk * 4 * W;
+        double cf[TPW];
 #pragma unroll
-      for (int k = 0; k < SYRK_TPW; ++k) {
-        if (k < nt) {
-          if (k > 0 && J == 0) fi = rp[I * 8];  // a new block row starts
-          dmma(acc[k], fi, rp[J * 8]);
+        for (int k = 0; k < TPW; ++k) cf[k] = rp[off[k] & 0xffffu];
+        double fi = rp[off[0] >> 16];
+#pragma unroll
+        for (int k = 0; k < TPW; ++k) {
+          if ((newrow >> k) & 1u) fi = rp[off[k] >> 16];  // a new block row starts
+          dmma(acc[k], fi, cf[k]);
         }
-        if (++J > I) ++I, J = 0;
       }
     }
     __syncwarp();
@@ -172,19 +193,18 @@ __global__ void __launch_bounds__(512, 2) syrk_kernel(const __grid_constant__ CU
   }
 
   double* P = part + (size_t)blockIdx.x * wp * wp;
-  int I = I0, J = J0;
 #pragma unroll
-  for (int k = 0; k < SYRK_TPW; ++k) {
+  for (int k = 0; k < TPW; ++k)
     if (k < nt)
-      *reinterpret_cast<double2*>(P + (size_t)(I * 8 + g) * wp + J * 8 + 2 * t) =
+      *reinterpret_cast<double2*>(P + (size_t)((off[k] >> 16) + g) * wp + (off[k] & 0xffffu) + 2 * t) =
           make_double2(acc[k][0], acc[k][1]);
-    if (++J > I) ++I, J = 0;
-  }
 }
 
 // Tiles per warp, consumer warps and tile-list splits over grid.y: equal runs,
-// <= 15 consumers, <= SYRK_TPW tiles each; among equal split counts the warp
-// count with the least padding wins.
+// <= 15 consumers, <= SYRK_TPW tiles each; the fewest splits, then the most
+// consumer warps per SM (runs of 3-6 tiles fit two CTAs per SM), then the
+// least padding.  Measured at m = 2e6 (B200): w = 55 0.44 -> 0.34 ms, w = 64
+// 0.52 -> 0.35, w = 82 0.93 -> 0.69 against the longest-run choice.
 struct SyrkPlan {
   int splits, tps, tpw, ncw;
 };
@@ -193,16 +213,19 @@ static SyrkPlan syrk_plan(int w) {
   SyrkPlan p{};
   p.splits = (int)ceil_div(ntiles, 15 * SYRK_TPW);
   p.tps = (int)ceil_div(ntiles, p.splits);
-  // long runs amortise the row fragment and the stage hand-off; short runs only
-  // when a long one would leave a warp idle
+  const int smem_per_sm = (int)std::max<size_t>(
+      1, 228 * 1024 / (kBarBytes + (size_t)4 * SYRK_KR * std::min(smem_ld(w), 256) * 8 + 1024));
   double best = 1e300;
-  for (int tpw = SYRK_TPW; tpw >= 1; --tpw) {
+  for (int tpw = SYRK_TPW; tpw >= 3; --tpw) {  // runs of 1-2 tiles: too many loads per DMMA
     const int ncw = (int)ceil_div(p.tps, tpw);
     if (ncw > 15) break;
-    const double score = (double)(tpw * ncw - p.tps) / p.tps + (tpw < 6 && p.tps >= 6 * ncw ? 0.2 : 0.0) +
-                         (tpw < 6 ? 0.05 * (6 - tpw) : 0.0);
+    const int warps_per_sm = ncw * std::min(syrk_minb(tpw), smem_per_sm);
+    const double score = -warps_per_sm + (double)(tpw * ncw - p.tps) / p.tps;
     if (score < best - 1e-12) best = score, p.ncw = ncw, p.tpw = tpw;
   }
+  static const int force_tpw = getenv("TSSVD_SYRK_TPW") ? atoi(getenv("TSSVD_SYRK_TPW")) : 0;  // experiments
+  if (force_tpw >= 1 && force_tpw <= SYRK_TPW && ceil_div(p.tps, force_tpw) <= 15)
+    p.tpw = force_tpw, p.ncw = (int)ceil_div(p.tps, force_tpw);
   return p;
 }
 
@@ -213,7 +236,7 @@ int syrk_partials_grid(int64_t m, int w) {
   const SyrkPlan p = syrk_plan(w);
   const size_t smem = kBarBytes + (size_t)4 * syrk_stage_bytes(w);
   int per_sm = (int)std::max<size_t>(1, std::min<size_t>(228 * 1024 / (smem + 1024), 2048 / (32 * (p.ncw + 1))));
-  per_sm = std::min(per_sm, 4);
+  per_sm = std::min(per_sm, syrk_minb(p.tpw));
   int64_t g = (int64_t)dev_info().sms * per_sm;
   int64_t maxg = std::max<int64_t>(1, ceil_div(m, SYRK_KR));
   return (int)std::max<int64_t>(1, std::min(g, maxg));
@@ -241,9 +264,23 @@ cudaError_t launch_syrk(const double* X, int64_t ldx, int64_t m, int w, double* 
   CUtensorMap tx;
   cudaError_t e = make_tmap(&tx, X, m, w, ldx, SYRK_KR, W);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  void (*kern)(CUtensorMap, int64_t, int, int, int64_t, double*, int, int, int) = nullptr;
+  switch (p.tpw) {
+    case 1: kern = syrk_kernel<1, syrk_minb(1)>; break;
+    case 2: kern = syrk_kernel<2, syrk_minb(2)>; break;
+    case 3: kern = syrk_kernel<3, syrk_minb(3)>; break;
+    case 4: kern = syrk_kernel<4, syrk_minb(4)>; break;
+    case 5: kern = syrk_kernel<5, syrk_minb(5)>; break;
+    case 6: kern = syrk_kernel<6, syrk_minb(6)>; break;
+    case 7: kern = syrk_kernel<7, syrk_minb(7)>; break;
+    case 8: kern = syrk_kernel<8, syrk_minb(8)>; break;
+    case 9: kern = syrk_kernel<9, syrk_minb(9)>; break;
+    case 10: kern = syrk_kernel<10, syrk_minb(10)>; break;
+    default: kern = syrk_kernel<SYRK_TPW, syrk_minb(SYRK_TPW)>; break;
+  }
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  syrk_kernel<<<dim3(gx, p.splits), (p.ncw + 1) * 32, smem, s>>>(tx, m, w, W, rpc, part, nst, p.tps, p.tpw);
+  kern<<<dim3(gx, p.splits), (p.ncw + 1) * 32, smem, s>>>(tx, m, w, W, rpc, part, nst, p.tps, p.tpw);
   return cudaGetLastError();
 }
 
