@@ -200,28 +200,39 @@ __global__ void __launch_bounds__(512, MINB) syrk_kernel(const __grid_constant__
           make_double2(acc[k][0], acc[k][1]);
 }
 
-// Tiles per warp, consumer warps and tile-list splits over grid.y: equal runs,
-// <= 15 consumers, <= SYRK_TPW tiles each; the fewest splits, then the most
-// consumer warps per SM (runs of 3-6 tiles fit two CTAs per SM), then the
-// least padding.  Measured at m = 2e6 (B200): w = 55 0.44 -> 0.34 ms, w = 64
-// 0.52 -> 0.35, w = 82 0.93 -> 0.69 against the longest-run choice.
+// Tiles per warp, consumer warps and tile-list splits over grid.y: equal runs
+// of 3..SYRK_TPW tiles, <= 15 consumer warps.  The DMMA pipe belongs to an SM
+// sub-partition (warp w runs on SMSP w % 4), and every stage waits for the
+// slowest warp, so a CTA's time per stage is ceil(ncw / 4) * tpw DMMA slots on
+// its busiest SMSP: the planner maximises
+//   (useful tiles / DMMA slots) x min(1, consumer warps per SMSP / 3) x 0.93^(splits-1),
+// the second factor for latency hiding (runs of <= 6 tiles fit two CTAs per
+// SM), the third for re-streaming the rows once per split.  Measured at
+// m = 2e6 (B200, tools/gram_bench.py): it picks the fastest of the measured
+// shapes at w = 55, 64, 82, 92, 100 (0.32, 0.35, 0.64, 0.70, 0.81 ms; w = 100
+// was 13 x 7 = 0.91 ms).
 struct SyrkPlan {
   int splits, tps, tpw, ncw;
 };
 static SyrkPlan syrk_plan(int w) {
   const int nb = (w + 7) / 8, ntiles = nb * (nb + 1) / 2;
-  SyrkPlan p{};
-  p.splits = (int)ceil_div(ntiles, 15 * SYRK_TPW);
-  p.tps = (int)ceil_div(ntiles, p.splits);
   const int smem_per_sm = (int)std::max<size_t>(
       1, 228 * 1024 / (kBarBytes + (size_t)4 * SYRK_KR * std::min(smem_ld(w), 256) * 8 + 1024));
-  double best = 1e300;
-  for (int tpw = SYRK_TPW; tpw >= 3; --tpw) {  // runs of 1-2 tiles: too many loads per DMMA
-    const int ncw = (int)ceil_div(p.tps, tpw);
-    if (ncw > 15) break;
-    const int warps_per_sm = ncw * std::min(syrk_minb(tpw), smem_per_sm);
-    const double score = -warps_per_sm + (double)(tpw * ncw - p.tps) / p.tps;
-    if (score < best - 1e-12) best = score, p.ncw = ncw, p.tpw = tpw;
+  SyrkPlan p{};
+  double best = -1.0;
+  static const int force_splits = getenv("TSSVD_SYRK_SPLITS") ? atoi(getenv("TSSVD_SYRK_SPLITS")) : 0;
+  const int s0 = std::max((int)ceil_div(ntiles, 15 * SYRK_TPW), force_splits);
+  for (int splits = s0; splits <= (force_splits ? s0 : s0 + 1); ++splits) {
+    const int tps = (int)ceil_div(ntiles, splits);
+    for (int tpw = SYRK_TPW; tpw >= 3; --tpw) {  // runs of 1-2 tiles: too many loads per DMMA
+      const int ncw = (int)ceil_div(tps, tpw);
+      if (ncw > 15) break;
+      const int per_sm = std::min(syrk_minb(tpw), smem_per_sm);
+      const double slots = (double)splits * 4 * ceil_div(ncw, 4) * tpw;
+      const double score = ntiles / slots * std::min(1.0, ncw * per_sm / 4.0 / 3.0) *
+                           std::pow(0.93, splits - 1);  // every split re-streams the rows
+      if (score > best + 1e-9) best = score, p.splits = splits, p.tps = tps, p.ncw = ncw, p.tpw = tpw;
+    }
   }
   static const int force_tpw = getenv("TSSVD_SYRK_TPW") ? atoi(getenv("TSSVD_SYRK_TPW")) : 0;  // experiments
   if (force_tpw >= 1 && force_tpw <= SYRK_TPW && ceil_div(p.tps, force_tpw) <= 15)
