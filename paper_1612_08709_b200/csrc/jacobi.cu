@@ -790,9 +790,10 @@ static size_t jac_smem(int C, int nslots, int P) {
 // cycles per warp-instruction on the 16-lane FP64 unit, SHFL+DADD 35, LDS 29,
 // shared-memory bandwidth 128 B/cycle/SM, MUFU f64 ~19; the rotation
 // parameters ~230 on the critical path; a cluster round adds an st.async
-// exchange through DSMEM and an mbarrier wait: measured ~1400 more than the
-// shared-memory traffic it saves, so clusters only when one CTA cannot hold
-// the columns).  A round reads and writes both columns of
+// exchange through DSMEM and an mbarrier wait that grows with the cluster:
+// measured ~1400 cycles at C = 2 and 2100 more at C = 8 than at C = 4
+// (n = 200: 6950 vs 4840 cycles per round), modelled as 700 C; so clusters
+// only when one CTA cannot hold the columns, and the smallest that can).  A round reads and writes both columns of
 // every pair, so one CTA is shared-memory-bandwidth bound.
 static double jac_round_cost(int C, int G, int V, int npairs) {
   const int warps = (int)ceil_div(npairs, 32 / G);
@@ -802,7 +803,7 @@ static double jac_round_cost(int C, int G, int V, int npairs) {
   const double pipe = 2.0 * per_smsp * (14.0 * V + 3.0 * lg + 35.0);
   const double smem = 2.0 * npairs * (2.0 * G * V) * 16.0 / 128.0 / C;
   const double chain = 60.0 + 9.0 * V + 35.0 * lg + 230.0 + 16.0 * V;
-  return std::max(pipe, smem) + chain + (C > 1 ? 1400.0 : 50.0);  // cluster: calibrated on B200
+  return std::max(pipe, smem) + chain + (C > 1 ? 700.0 * C : 50.0);  // cluster: calibrated on B200
 }
 
 static cudaError_t jac_dispatch(JacArgs a, cudaStream_t s) {
