@@ -17,6 +17,17 @@ if timeout 600 $CMD > $O/plain.log 2>&1; then
 fi
 CMD2="python tools/profile_step.py --config c2 --steps 2"
 if timeout 600 $CMD2 > $O/plain2.log 2>&1; then
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"syrk|gemm_nn|jacobi" -s 8 -c 8 -o $O/prof $CMD2 > $O/ncu_full.log 2>&1
+  timeout 1200 ncu --set full --clock-control none -k regex:"syrk|gemm_nn|jacobi" -s 8 -c 8 -o $O/prof $CMD2 > $O/ncu_full.log 2>&1
+  python tools/ncu_summary.py $O/prof.ncu-rep > $O/ncu_full_summary.txt 2>&1
 fi
 echo done > $O/DONE
+# c4: full capture of the Gram and GEMM passes (roofline.traffic of `bench.py --config c4`)
+if [ "${SKIP_C4:-0}" = 0 ]; then
+timeout 900 python bench.py --config c4 --no-cpu-baseline > $O/bench_c4.json 2> $O/bench_c4.err; echo "exit $?" >> $O/bench_c4.err
+CMD3="python tools/profile_step.py --config c4 --steps 1"
+timeout 1500 ncu --set full --clock-control none -k regex:"syrk|gemm_nn" -c 2 -o $O/prof_c4 $CMD3 > $O/ncu_full_c4.log 2>&1
+python tools/ncu_summary.py $O/prof_c4.ncu-rep > $O/ncu_full_c4_summary.txt 2>&1
+fi
+# gpurun brings back <= 64 MiB: keep the summaries, drop large reports
+find $O -name '*.ncu-rep' -size +20M -delete
+echo done2 > $O/DONE2
