@@ -577,7 +577,12 @@ static NnShape nn_shape(int c) {
   NnShape sh;
   sh.xr = nn_xr(c);
   sh.ni = sh.xr ? c / 8 : (c + 7) / 8;
-  sh.wc = sh.ni <= 16 ? 1 : 2;
+  // two column groups from 12 column blocks on: each warp then holds 3 x 6..8
+  // tiles instead of 1 x 12..16, 0.5 instead of 1.07 fragment loads per DMMA
+  // (c4 A V~ 13.36 -> 13.14 ms); below 12 the padded column block costs more
+  // (c2, 9 blocks: 1.02 -> 1.09 ms).  TSSVD_NN_WC2 moves the threshold (experiments).
+  static const int wc2_from = getenv("TSSVD_NN_WC2") ? atoi(getenv("TSSVD_NN_WC2")) : 12;
+  sh.wc = sh.ni < wc2_from || sh.xr ? 1 : 2;
   sh.niw = (sh.ni + sh.wc - 1) / sh.wc;
   sh.mi = std::max(1, std::min(4, 24 / sh.niw));
   return sh;
@@ -643,10 +648,10 @@ static cudaError_t nn_go(const NnPlan& p, const CUtensorMap& tx, const CUtensorM
   return cudaGetLastError();
 }
 
-template <int NI, int XR = 0>
+template <int NI, int XR = 0, int WCF = 0>
 static cudaError_t nn_ni_go(const NnPlan& p, const CUtensorMap& tx, const CUtensorMap& tm, int64_t m,
                             int k, int c, double* Y, int64_t ldy, double* np, cudaStream_t s) {
-  constexpr int WC = NI <= 16 ? 1 : 2;
+  constexpr int WC = WCF ? WCF : (NI <= 16 ? 1 : 2);
   constexpr int NIW = (NI + WC - 1) / WC;
   constexpr int MI = 24 / NIW < 1 ? 1 : (24 / NIW > 4 ? 4 : 24 / NIW);
   return nn_go<MI, NIW, WC, XR>(p, tx, tm, m, k, c, Y, ldy, np, s);
@@ -674,6 +679,13 @@ cudaError_t launch_gemm_nn(const double* X, int64_t ldx, int64_t m, int k, const
       default: return cudaErrorInvalidValue;
     }
 #undef NN_XCASE
+#define NN_WCASE(N) \
+  case N: return nn_ni_go<N, 0, 2>(p, tx, tm, m, k, c, Y, ldy, norm_part, s);
+  if (p.sh.wc == 2 && p.ni <= 16) switch (p.ni) {
+      NN_WCASE(9) NN_WCASE(10) NN_WCASE(11) NN_WCASE(12) NN_WCASE(13) NN_WCASE(14) NN_WCASE(15) NN_WCASE(16)
+      default: return cudaErrorInvalidValue;
+    }
+#undef NN_WCASE
 #define NN_CASE(N) \
   case N: return nn_ni_go<N>(p, tx, tm, m, k, c, Y, ldy, norm_part, s);
   switch (p.ni) {
