@@ -63,6 +63,16 @@ int tssvd_get_unique_id(unsigned char id[128]);
 /* Collective over `nranks` processes: ncclCommInitRank on `device`. */
 int tssvd_comm_create(int nranks, int rank, const unsigned char id[128], int device,
                       tssvd_comm** out);
+/* Borrow an existing NCCL communicator (an ncclComm_t, e.g. the one behind a
+ * torch ProcessGroupNCCL: pg._get_backend(torch.device("cuda"))._comm_ptr()).
+ * Rank, size and device are queried from NCCL.  The handle does not own the
+ * communicator: tssvd_comm_destroy frees only the handle, the caller keeps
+ * the communicator alive while the handle is in use.  Same NCCL library
+ * required (the process's libnccl.so.2).  Errors: TSSVD_EINVAL for a NULL
+ * communicator or out pointer, TSSVD_ENCCL when NCCL rejects the queries. */
+int tssvd_comm_wrap_nccl(void* nccl_comm, tssvd_comm** out);
+/* Frees the handle; destroys the NCCL communicator only if it was created by
+ * tssvd_comm_create. */
 int tssvd_comm_destroy(tssvd_comm* comm);
 int tssvd_comm_rank(const tssvd_comm* comm, int* rank, int* nranks);
 /* Sum-allreduce of `count` doubles in place on `stream` (exposed for tests). */

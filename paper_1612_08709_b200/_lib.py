@@ -47,6 +47,7 @@ SIGNATURES = [
     ("tssvd_abi_version", c_int, []),
     ("tssvd_get_unique_id", c_int, [P(ctypes.c_ubyte)]),
     ("tssvd_comm_create", c_int, [c_int, c_int, P(ctypes.c_ubyte), c_int, P(c_void_p)]),
+    ("tssvd_comm_wrap_nccl", c_int, [c_void_p, P(c_void_p)]),
     ("tssvd_comm_destroy", c_int, [c_void_p]),
     ("tssvd_comm_rank", c_int, [c_void_p, P(c_int), P(c_int)]),
     ("tssvd_allreduce_sum", c_int, [c_void_p, c_void_p, c_void_p, c_int64]),

@@ -53,6 +53,20 @@ class Comm:
         check(lib().tssvd_comm_create(self.world, self.rank, uid, self.device,
                                       ctypes.byref(self.handle)))
 
+    @classmethod
+    def from_nccl(cls, nccl_comm_ptr: int) -> "Comm":
+        """Borrow an existing ncclComm_t (e.g. ``pg._get_backend(torch.device("cuda"))._comm_ptr()``
+        of an initialised ProcessGroupNCCL) instead of creating a second communicator; the
+        caller keeps that communicator alive."""
+        self = cls.__new__(cls)
+        self.handle = ctypes.c_void_p(None)
+        check(lib().tssvd_comm_wrap_nccl(ctypes.c_void_p(nccl_comm_ptr), ctypes.byref(self.handle)))
+        r, w = ctypes.c_int(), ctypes.c_int()
+        check(lib().tssvd_comm_rank(self.handle, ctypes.byref(r), ctypes.byref(w)))
+        self.rank, self.world = r.value, w.value
+        self.device = torch.cuda.current_device()
+        return self
+
     @property
     def ptr(self):
         return self.handle.value

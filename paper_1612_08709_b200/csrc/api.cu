@@ -22,6 +22,7 @@
 struct tssvd_comm {
   ncclComm_t nccl = nullptr;
   int rank = 0, nranks = 1, device = 0;
+  bool owned = true;  // false: borrowed through tssvd_comm_wrap_nccl
 };
 
 namespace {
@@ -720,10 +721,27 @@ int tssvd_comm_create(int nranks, int rank, const unsigned char id[128], int dev
   });
 }
 
+int tssvd_comm_wrap_nccl(void* nccl_comm, tssvd_comm** out) {
+  return guarded([&] {
+    if (!nccl_comm || !out) fail(TSSVD_EINVAL, "tssvd_comm_wrap_nccl: NULL communicator or out pointer");
+    auto* c = new tssvd_comm;
+    c->nccl = static_cast<ncclComm_t>(nccl_comm);
+    c->owned = false;
+    ncclResult_t r = ncclCommUserRank(c->nccl, &c->rank);
+    if (r == ncclSuccess) r = ncclCommCount(c->nccl, &c->nranks);
+    if (r == ncclSuccess) r = ncclCommCuDevice(c->nccl, &c->device);
+    if (r != ncclSuccess) {
+      delete c;
+      fail(TSSVD_ENCCL, "tssvd_comm_wrap_nccl: %s", ncclGetErrorString(r));
+    }
+    *out = c;
+  });
+}
+
 int tssvd_comm_destroy(tssvd_comm* c) {
   return guarded([&] {
     if (!c) return;
-    if (c->nccl) NC(ncclCommDestroy(c->nccl));
+    if (c->nccl && c->owned) NC(ncclCommDestroy(c->nccl));
     delete c;
   });
 }

@@ -21,7 +21,8 @@ def declared_functions():
 def test_header_declares_expected_entry_points():
     names = declared_functions()
     for must in ("tssvd", "lowrank_svd", "tssvd_workspace_size", "lowrank_workspace_size",
-                 "tssvd_comm_create", "tssvd_get_unique_id", "tssvd_status_string"):
+                 "tssvd_comm_create", "tssvd_comm_wrap_nccl", "tssvd_get_unique_id",
+                 "tssvd_status_string"):
         assert must in names
 
 
@@ -54,6 +55,8 @@ def test_workspace_queries_and_validation_without_gpu():
     assert h.tssvd_workspace_size(None, 100, 10, ctypes.byref(bad), ctypes.byref(nb)) == 1
     assert b"working precision" in h.tssvd_last_error()
     assert h.lowrank_workspace_size(None, 100, 50, 50, ctypes.byref(o), ctypes.byref(nb)) == 1
+    out = ctypes.c_void_p()
+    assert h.tssvd_comm_wrap_nccl(None, ctypes.byref(out)) == 1 and not out.value  # NULL comm: EINVAL
 
 
 def test_no_cpu_fallback_in_product_package():

@@ -333,3 +333,26 @@ def test_lowrank_l128():
     eg = oracle.spectral_error(a, *gpu, x0)
     er = oracle.spectral_error(a, *ref, x0)
     assert abs(eg - er) <= 0.01 * er
+
+
+def test_comm_wrap_nccl_borrows_torch_communicator():
+    """tssvd_comm_wrap_nccl on the ncclComm_t of a (world-size-1) ProcessGroupNCCL: the call
+    through the borrowed communicator gives bit-identical results to the comm-less call, and
+    destroying the handle leaves torch's communicator usable."""
+    import torch.distributed as dist
+
+    store = dist.HashStore()
+    pg = dist.ProcessGroupNCCL(store, 0, 1)
+    x = torch.ones(4, device=DEV)
+    pg.allreduce([x]).wait()  # the NCCL communicator exists from the first collective on
+    ptr = pg._comm_ptr() if hasattr(pg, "_comm_ptr") else pg._get_backend(DEV)._comm_ptr()
+    comm = tk.Comm.from_nccl(ptr)
+    assert (comm.rank, comm.world) == (0, 1)
+    d = synth.config_inputs("c1")
+    r1 = run_tssvd(d["A"], 1e-11, 2, comm=comm)
+    r0 = run_tssvd(d["A"], 1e-11, 2)
+    for a, b in zip(r1, r0):
+        assert np.array_equal(a, b)
+    comm.close()
+    pg.allreduce([x]).wait()
+    assert torch.equal(x.cpu(), torch.ones(4))
