@@ -126,6 +126,16 @@ def a_passes(cfg):
 
 
 # ------------------------------------------------------------ reference --
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def run_reference(args, rank, world):
     """--impl reference: the oracle (oracle/) as it stands, on the host cores, bounded samples."""
     if rank != 0:
@@ -146,10 +156,11 @@ def run_reference(args, rank, world):
 
     for _ in range(args.warmup):
         step()
-    t0 = time.perf_counter()
+    t0, c0 = time.perf_counter(), time.process_time()
     for _ in range(args.steps):
         step()
     dt = (time.perf_counter() - t0) / args.steps
+    cpu_s = (time.process_time() - c0) / args.steps
     gbs = a_passes(cfg) * a.nbytes / dt / 1e9
     sample = f"first {a.shape[0]} rows x {a.shape[1]} cols of {args.config} ({a.nbytes / 1e9:.2f} GB)"
     line = {"impl": "reference", "metric": metric_name(cfg), "value": round(gbs, 3), "unit": "GB/s",
@@ -158,7 +169,8 @@ def run_reference(args, rank, world):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_obj(args, cfg, world),
             "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": os.cpu_count(),
-                             "kind": "oracle", "sample": sample},
+                             "kind": "oracle", "sample": sample, "cpu_model": cpu_model(),
+                             "wall_s_per_step": round(dt, 3), "cpu_s_per_step": round(cpu_s, 3)},
             "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -313,7 +325,7 @@ def cpu_baseline(args, cfg):
     d = synth.config_inputs(args.config, m=min(rows, cfg["m"]),
                             n=None if cfg["kind"] == "tssvd" else min(cfg["n"], 4_000))
     a = d["A"]
-    reps, t0 = 0, time.perf_counter()
+    reps, t0, c0 = 0, time.perf_counter(), time.process_time()
     while True:
         if cfg["kind"] == "tssvd":
             oracle.tssvd(a, args.wp, 2)
@@ -323,8 +335,10 @@ def cpu_baseline(args, cfg):
         if time.perf_counter() - t0 > 10.0 or reps >= 20:
             break
     dt = (time.perf_counter() - t0) / reps
+    cpu_s = (time.process_time() - c0) / reps
     return {"value": round(a_passes(cfg) * a.nbytes / dt / 1e9, 3), "unit": "GB/s",
-            "cores": os.cpu_count(), "kind": "oracle",
+            "cores": os.cpu_count(), "kind": "oracle", "cpu_model": cpu_model(),
+            "wall_s_per_step": round(dt, 3), "cpu_s_per_step": round(cpu_s, 3),
             "sample": f"{reps} oracle runs on the first {a.shape[0]} rows x {a.shape[1]} cols of "
                       f"{args.config} ({a.nbytes / 1e9:.2f} GB), {dt:.2f} s each"}
 
