@@ -186,6 +186,19 @@ __device__ __forceinline__ void dots8(const double2 (&x)[V], const double2 (&y)[
   }
 }
 
+#ifdef JAC_PROF  // phase timing of the element rounds (tools/jac_phase.cu only)
+__device__ unsigned long long g_jac_phase[8];
+#define JP_DECL long long jp_t[5] = {0, 0, 0, 0, 0};
+#define JP_T(i) if (threadIdx.x == 0) jp_t[i] = clock64();
+#define JP_ACC                                                                     \
+  if (threadIdx.x == 0)                                                            \
+    for (int i = 1; i < 5; ++i) atomicAdd(&g_jac_phase[i], (unsigned long long)(jp_t[i] - jp_t[i - 1]));
+#else
+#define JP_DECL
+#define JP_T(i)
+#define JP_ACC
+#endif
+
 template <int C, int G, int V, bool BLK>
 __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
   Cl<C> cl;
@@ -619,6 +632,8 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
   for (; sweep < a.max_sweeps && !converged; ++sweep) {
     int any = 0;
     for (int r = 0; r < NE - 1; ++r, ++rounds) {
+      JP_DECL
+      JP_T(0)
       int rot = 0;
       double al = 0.0, be = 0.0, ga = 0.0;
       double2 vp[V], vq[V];
@@ -644,12 +659,14 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
         al += al1;
         be += be1;
         ga += ga1;
+        JP_T(1)
 #pragma unroll
         for (int o = G / 2; o > 0; o >>= 1) {  // xor butterfly: identical sums in every lane
           al += __shfl_xor_sync(gmask, al, o);
           be += __shfl_xor_sync(gmask, be, o);
           ga += __shfl_xor_sync(gmask, ga, o);
         }
+        JP_T(2)
       }
       if constexpr (C > 1) {
         // partial dot products to every CTA of the cluster: plain stores locally, st.async
@@ -688,7 +705,10 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
       // advance this pair's positions to the next round
       if (pos_p != 0) pos_p = pos_p == NE - 1 ? 1 : pos_p + 1;
       pos_q = pos_q == NE - 1 ? 1 : pos_q + 1;
+      JP_T(3)
       any |= __syncthreads_or(rot);
+      JP_T(4)
+      JP_ACC
     }
     converged = !any;
   }
