@@ -11,6 +11,10 @@ import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libtssvd_b200.so")
+# A/B experiments: load another build of the same library (no rebuild check)
+_LIB_OVERRIDE = os.environ.get("TSSVD_LIB")
+if _LIB_OVERRIDE:
+    LIB_PATH = _LIB_OVERRIDE
 
 c_int, c_int64, c_double, c_size_t = ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_size_t
 c_void_p, c_char_p = ctypes.c_void_p, ctypes.c_char_p
@@ -95,7 +99,7 @@ def lib() -> ctypes.CDLL:
             from . import build as _build
 
             try:
-                if _build.needs_build():
+                if not _LIB_OVERRIDE and _build.needs_build():
                     _build.build()
             except Exception as e:  # no toolchain: the existing .so (if any) must do
                 if not os.path.exists(LIB_PATH):

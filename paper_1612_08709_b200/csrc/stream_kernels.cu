@@ -709,7 +709,7 @@ cudaError_t launch_gemm_nn(const double* X, int64_t ldx, int64_t m, int k, const
 // XR > 0 (l = 8 NBL + XR): the last XR columns of Y on the FMA pipe, as in gemm_nn
 // (lane (g, t) holds X[4kk + t][i0 + g] as its A fragment; the four t-partials
 // are summed by a butterfly before the store).
-static constexpr int TN_CW = 8;
+static constexpr int TN_CW = 12;  // 3 consumer warps per SMSP: 8 -> 12 took c3 beta 7.7 -> 6.7 ms/pass
 
 template <int MI, int NBL, int XR>
 __global__ void __launch_bounds__(32 * (TN_CW + 1)) gemm_tn_kernel(
