@@ -380,9 +380,11 @@ cudaError_t launch_reduce_parts(const double* part, int np, int64_t stride, int6
 // broadcast M[4 kk + t][8 NIW + x] and the four t-partials are summed by an xor
 // butterfly at the end of the tile (c = 25 = 3*8 + 1: 25 instead of 32 columns
 // of FP64 work).
-static constexpr int NN_CW = 8;  // consumer warps
+// Consumer warps: 12 (3 per SMSP) when a warp's accumulators are small
+// (MI * NIW <= 12 tiles, one column group: register room for 13 warps), else 8.
+__host__ __device__ constexpr int nn_cw(int mi, int niw, int wc) { return mi * niw <= 12 && wc == 1 ? 12 : 8; }
 
-template <int MI, int NIW, int WC, int XR>
+template <int MI, int NIW, int WC, int XR, int NN_CW = nn_cw(MI, NIW, WC)>
 __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
     const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tm, int64_t m, int k,
     int KC, int kc_count, int LDM, int c, double* Y, int64_t ldy, double* __restrict__ norm_part,
@@ -412,7 +414,11 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
         const int k0 = (int)(s % kc_count) * KC;
         double* xs = buf + b * stage_d;
         mbar_arrive_expect_tx(ring.full(b), (uint32_t)(stage_d * 8));
-        tma_load_2d(xs, &tx, k0, (int)(tile * R), ring.full(b));
+        // the X box in TMA boxes of at most 256 rows (R = 384 with 12 consumer warps)
+        constexpr int RB = R <= 256 ? R : R / 2;
+#pragma unroll
+        for (int h = 0; h < R / RB; ++h)
+          tma_load_2d(xs + h * RB * KC, &tx, k0, (int)(tile * R + h * RB), ring.full(b));
         tma_load_2d(xs + xs_d, &tm, 0, k0, ring.full(b));
       }
     return;
@@ -601,9 +607,10 @@ static NnPlan plan_nn(int64_t m, int k, int c) {
   NnPlan p;
   p.sh = nn_shape(c);
   p.ni = p.sh.ni;
-  p.R = 8 * p.sh.mi * (NN_CW / p.sh.wc);
+  const int ncw = nn_cw(p.sh.mi, p.sh.niw, p.sh.wc);
+  p.R = 8 * p.sh.mi * (ncw / p.sh.wc);
   p.ldm = std::min(smem_ld(c), 256);  // smem row stride of the M box (TMA box limit)
-  const size_t red = (size_t)NN_CW * (p.sh.niw + (p.sh.xr > 0)) * 8 * 8;
+  const size_t red = (size_t)ncw * (p.sh.niw + (p.sh.xr > 0)) * 8 * 8;
   const size_t budget = dev_info().smem_optin - kBarBytes - red;
   double best = 1e300;
   p.KC = 28;
@@ -628,7 +635,7 @@ static NnPlan plan_nn(int64_t m, int k, int c) {
 
 int gemm_nn_grid(int64_t m, int c) {
   const NnShape sh = nn_shape(c);
-  const int R = 8 * sh.mi * (NN_CW / sh.wc);
+  const int R = 8 * sh.mi * (nn_cw(sh.mi, sh.niw, sh.wc) / sh.wc);
   return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, R), dev_info().sms));
 }
 int gemm_nn_part_stride(int c) {
@@ -643,7 +650,7 @@ static cudaError_t nn_go(const NnPlan& p, const CUtensorMap& tx, const CUtensorM
   auto kern = gemm_nn_kernel<MI, NIW, WC, XR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
   if (e != cudaSuccess) return e;
-  kern<<<p.grid, (NN_CW + 1) * 32, p.smem, s>>>(tx, tm, m, k, p.KC, p.kcc, p.ldm, c, Y, ldy, norm_part,
+  kern<<<p.grid, (nn_cw(MI, NIW, WC) + 1) * 32, p.smem, s>>>(tx, tm, m, k, p.KC, p.kcc, p.ldm, c, Y, ldy, norm_part,
                                                 p.nst);
   return cudaGetLastError();
 }
@@ -667,7 +674,7 @@ cudaError_t launch_gemm_nn(const double* X, int64_t ldx, int64_t m, int k, const
     return cudaSuccess;
   }
   CUtensorMap tx, tm;
-  cudaError_t e = make_tmap(&tx, X, m, k, ldx, p.R, p.KC);
+  cudaError_t e = make_tmap(&tx, X, m, k, ldx, p.R <= 256 ? p.R : p.R / 2, p.KC);
   if (e != cudaSuccess) return e;
   e = make_tmap(&tm, M, k, smem_ld(c), smem_ld(c), p.KC, p.ldm);
   if (e != cudaSuccess) return e;
