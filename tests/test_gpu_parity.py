@@ -141,6 +141,30 @@ def test_tssvd_c2_full_size():
     print(info)
 
 
+@pytest.mark.slow
+def test_tssvd_c4_full_size_properties():
+    """BASELINE configs[3] at full size (8e6 x 200, cond 1e12), the `bench.py --config c4`
+    workload: properties that hold at any size (the oracle would need ~40 GB of host memory):
+    the predicted kept rank (92), sigma against the constructed spectrum, U and V
+    orthonormal after the second pass, and the rank-r reconstruction on sampled rows."""
+    d = synth.config_inputs("c4")
+    A = to_dev(d["A"])
+    del d["A"]
+    u, s, v = tk.tssvd(A, wp=1e-11, passes=2)
+    torch.cuda.synchronize()
+    r = s.numel()
+    assert r == 92
+    sig = d["sigma"]
+    assert torch.max(torch.abs(s.cpu() - torch.from_numpy(sig[:r]))).item() <= 1e-10 * sig[0]
+    eye = torch.eye(r, dtype=torch.float64, device=DEV)
+    assert torch.max(torch.abs(u.T @ u - eye)).item() <= 1e-13
+    assert torch.max(torch.abs(v.T @ v - eye)).item() <= 1e-13
+    rows = torch.from_numpy(np.random.default_rng(4).choice(A.shape[0], 4096, replace=False)).to(DEV)
+    resid = A[rows] - (u[rows] * s) @ v.T
+    # the discarded tail: sigma_{r+1} bounds the rank-r residual of every row
+    assert torch.max(torch.linalg.norm(resid, dim=1)).item() <= 1.01 * sig[r]
+
+
 @pytest.mark.parametrize("m,n", [(2, 2), (33, 32), (1000, 2), (12_345, 18), (70_001, 64), (4_097, 130),
                                  (9_999, 256)])
 def test_tssvd_ragged_random(m, n):
