@@ -60,6 +60,7 @@ struct JacArgs {
   int V;     // double2 per lane per slot in the sweeps (= template V)
   double tol, trunc;
   int max_sweeps;
+  int blk_min;  // warp-block ordering when more than blk_min columns survive the Cholesky
   double* out;
   int ldout;
   double* vals;
@@ -506,7 +507,7 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
   const long long t_chol = clock64();
   int sweep = 0, rounds = 0;
   bool converged = K <= 1;
-  if (BLK && C == 1 && K > 64 && K <= 8 * JW) {
+  if (BLK && C == 1 && K > a.blk_min && K <= 8 * JW) {
     // Warp-block ordering (one CTA).  The K columns are taken four at a time
     // ("blocks", padded to an even number of blocks with the zero slot).  In a
     // block round warp w holds the block pair (T, B) that the circle ordering
@@ -854,7 +855,9 @@ static cudaError_t jac_dispatch(JacArgs a, cudaStream_t s) {
   // survive the Cholesky, they fit one pass of the 16 warps and one CTA holds
   // them (TSSVD_JAC_BLK=0 disables; K <= 64 falls back to the element ordering)
   static const bool blk_ok = !getenv("TSSVD_JAC_BLK") || atoi(getenv("TSSVD_JAC_BLK")) != 0;
-  if (blk_ok && !force_g && force_c <= 1 && nslots > 64 && nslots <= 8 * JW) {
+  static const int blk_min = getenv("TSSVD_JAC_BLKMIN") ? atoi(getenv("TSSVD_JAC_BLKMIN")) : 64;
+  a.blk_min = blk_min;
+  if (blk_ok && !force_g && force_c <= 1 && nslots > blk_min && nslots <= 8 * JW) {
     const int V = std::max(2, (int)ceil_div(a.L, 16));
     if (V <= 8 && jac_smem(1, nslots, 16 * V) <= budget) {
       a.Lh = (a.L + 1) & ~1;
