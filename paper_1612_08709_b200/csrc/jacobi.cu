@@ -116,15 +116,7 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       : "memory");
 }
 
-// Reciprocal and reciprocal square root: MUFU approximation + two Newton steps.
-__device__ __forceinline__ double rcp_nr(double x) {
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-x, y, 1.0);
-  return fma(y, e, y);
-}
+// Reciprocal square root: MUFU approximation + two Newton steps.
 __device__ __forceinline__ double rsqrt_nr(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
@@ -141,8 +133,8 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
 // both columns are negligible.  With d = be - al:
 //   t = tan(theta) = sign(d) 2ga / (|d| + sqrt(d^2 + 4ga^2)),  c = 1/sqrt(1+t^2), s = c t;
 // then x_p' = c x_p - s x_q, x_q' = s x_p + c x_q.  d and 2ga are first scaled by
-// a power of two (exact) so the squares cannot over/underflow; reciprocal and
-// rsqrt by MUFU + two Newton steps (~1 ulp).
+// a power of two (exact) so the squares cannot over/underflow; rsqrt by MUFU +
+// two Newton steps (~1 ulp).
 __device__ __forceinline__ bool jac_rot(double al, double be, double ga, double tol2, double skip2,
                                         double& c, double& sn) {
   if (!(ga != 0.0 && ga * ga > tol2 * al * be && fmax(al, be) > skip2)) return false;
@@ -152,11 +144,18 @@ __device__ __forceinline__ bool jac_rot(double al, double be, double ga, double 
   const double sc = __longlong_as_double((long long)(2046 - ex) << 52);  // 2^(1023 - ex)
   d *= sc;
   g2 *= sc;
+  // With root = sqrt(d^2 + g2^2) and q = |d| + root:  c^2 = q / (2 root) and
+  // s = sign(d) g2 / sqrt(2 root q) (the same c, s as t = sign(d) g2 / q,
+  // c = 1/sqrt(1+t^2), s = c t), so the two reciprocal square roots run in
+  // parallel after the first instead of rsqrt -> rcp -> rsqrt in series.
   const double w = fma(d, d, g2 * g2);
-  const double root = w * rsqrt_nr(w);
-  const double t = (d >= 0.0 ? g2 : -g2) * rcp_nr(fabs(d) + root);
-  c = rsqrt_nr(fma(t, t, 1.0));
-  sn = c * t;
+  const double y = rsqrt_nr(w);  // 1 / root
+  const double root = w * y;
+  const double q = fabs(d) + root;
+  const double u = q * (0.5 * y);
+  const double v = (root + root) * q;
+  c = u * rsqrt_nr(u);
+  sn = (d >= 0.0 ? g2 : -g2) * rsqrt_nr(v);
   return true;
 }
 
