@@ -14,6 +14,7 @@ KEYS = [("gpu__time_duration.sum", "ms"), ("dram__bytes_read.sum", "dram_rd"),
         ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor%"),
         ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "fp64%"),
         ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue%"),
+        ("lts__t_sector_hit_rate.pct", "l2_hit%"),
         ("launch__registers_per_thread", "regs"), ("launch__grid_size", "grid"),
         ("launch__block_size", "block"),
         ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem_conflicts")]
