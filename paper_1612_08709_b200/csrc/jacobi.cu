@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
           const int p = bi;
           const double dp = bv;
           if (p < 0 || !(dp > tabs)) break;  // uniform over the CTA
-          const double rsq = 1.0 / sqrt(dp);
+          const double rsq = rsqrt_nr(dp);  // MUFU + Newton: no IEEE div / sqrt sequences on the pivot chain
           if ((p % JW) == warp) {  // owner of slot p: publish column p, write X[:, k]
             const int jp = p / JW;
 #pragma unroll
@@ -331,7 +331,7 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
           }
           if (tid == 0) s_order[k] = k;
           __syncthreads();
-          const double inv = 1.0 / dp;
+          const double inv = rsq * rsq;
           double pr[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
@@ -406,12 +406,13 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
         }
       }
       if (p < 0 || !(dp > tabs)) break;  // uniform over the cluster
+      const double rsq = rsqrt_nr(dp);
       if (tid == 0) {
         s_order[k] = p;
         s_rank[p] = 1;
-        s_nrm[k] = 1.0 / sqrt(dp);
+        s_nrm[k] = rsq;
       }
-      const double inv = 1.0 / dp;
+      const double inv = rsq * rsq;
       const double* fsrc = X + p * P;  // C == 1: S[s][p] = slot p, row s
       if constexpr (C > 1) {
         // the owner of row p broadcasts S[p][s] (row p of every slot) to the cluster
