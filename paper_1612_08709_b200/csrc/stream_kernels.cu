@@ -127,7 +127,10 @@ __global__ void __launch_bounds__(512, MINB) syrk_kernel(const __grid_constant__
   const int wp = nb * 8;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int ncw = (blockDim.x >> 5) - 1;  // consumer warps (warp 0 produces)
-  const int64_t r0 = (int64_t)blockIdx.x * rpc;
+  // grid = (tile-list splits, row blocks): the splits of one row block are
+  // launched together, so the second reads its rows from L2 instead of HBM
+  const int rb = blockIdx.y, sp = blockIdx.x;
+  const int64_t r0 = (int64_t)rb * rpc;
   const int64_t r1 = min(m, r0 + rpc);
   const int nsteps = r1 > r0 ? (int)ceil_div(r1 - r0, SYRK_KR) : 0;
   ring_init(ring, nst, ncw);
@@ -143,8 +146,8 @@ __global__ void __launch_bounds__(512, MINB) syrk_kernel(const __grid_constant__
     return;
   }
   // this warp's run of tiles [q0, q1) of the row-major lower triangle
-  const int q0 = min(ntiles, blockIdx.y * tps + (warp - 1) * tpw);
-  const int q1 = min(ntiles, min(blockIdx.y * tps + tps, q0 + tpw));
+  const int q0 = min(ntiles, sp * tps + (warp - 1) * tpw);
+  const int q1 = min(ntiles, min(sp * tps + tps, q0 + tpw));
   const int nt = q1 - q0;
   int I0 = 0;
   while ((I0 + 1) * (I0 + 2) / 2 <= q0) ++I0;
@@ -192,7 +195,7 @@ __global__ void __launch_bounds__(512, MINB) syrk_kernel(const __grid_constant__
     if (lane == 0) mbar_arrive(ring.empty(b));
   }
 
-  double* P = part + (size_t)blockIdx.x * wp * wp;
+  double* P = part + (size_t)rb * wp * wp;
 #pragma unroll
   for (int k = 0; k < TPW; ++k)
     if (k < nt)
@@ -291,7 +294,7 @@ cudaError_t launch_syrk(const double* X, int64_t ldx, int64_t m, int w, double* 
   }
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  kern<<<dim3(gx, p.splits), (p.ncw + 1) * 32, smem, s>>>(tx, m, w, W, rpc, part, nst, p.tps, p.tpw);
+  kern<<<dim3(p.splits, gx), (p.ncw + 1) * 32, smem, s>>>(tx, m, w, W, rpc, part, nst, p.tps, p.tpw);
   return cudaGetLastError();
 }
 
