@@ -82,14 +82,21 @@ struct Cl {
   }
 };
 
-// argmax over a warp: larger value wins, ties -> lower index (idx < 0 = none)
+// argmax over a warp of the pivot candidates (v, i), i < 0 = none: larger v wins,
+// ties -> lower index.  Positive doubles order like their bit patterns, so the
+// max is two 32-bit redux.sync (high word, then low word among the high-word
+// winners) and the index a third (min over the winners) -- three reductions
+// instead of a 5-level shuffle butterfly over (double, int) pairs.  Candidates
+// <= 0 collapse to key 0 (the Cholesky stops there anyway: v = 0 is returned).
 __device__ __forceinline__ void warp_argmax(double& v, int& i) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, i, o);
-    if (oi >= 0 && (i < 0 || ov > v || (ov == v && oi < i))) v = ov, i = oi;
-  }
+  const unsigned long long key =
+      (i >= 0 && v > 0.0) ? static_cast<unsigned long long>(__double_as_longlong(v)) : 0ull;
+  const unsigned hi = static_cast<unsigned>(key >> 32), lo = static_cast<unsigned>(key);
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  const bool win = i >= 0 && hi == mhi && lo == mlo;
+  i = static_cast<int>(__reduce_min_sync(0xffffffffu, win ? static_cast<unsigned>(i) : 0xffffffffu));
+  v = __longlong_as_double(static_cast<long long>((static_cast<unsigned long long>(mhi) << 32) | mlo));
 }
 
 // DSMEM producer/consumer exchange: remote shared address of `p` in CTA `rank`,
