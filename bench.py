@@ -1,10 +1,13 @@
 """Benchmark of the Gram-based SVD hot path on B200 (driver contract: one JSON line).
 
-  python bench.py [--gpus N --steps K --warmup W] [--config c2] [--impl ours|reference]
+  python bench.py [--gpus N --steps K --warmup W] [--config c3] [--impl ours|reference]
 
-A "step" is one whole tall-skinny SVD (Algorithm 4, two Gram passes) of the
-BASELINE.json configs[1] matrix (2,000,000 x 100 FP64, Haar U/V, sigma from 1
-to 1e-10), row-sharded over N GPUs (strong scaling: the matrix is fixed).
+A "step" is one whole call of the hot path on a BASELINE.json config, row-sharded
+over N GPUs (strong scaling: the matrix is fixed).  Default: configs[2] (c3:
+200,000 x 20,000 FP64, 32 GB, Alg. 8 randomized low-rank SVD, k=20 l=25 i=2) --
+BASELINE's metric names no config, so the N=1 line runs the largest config that
+fits one GPU's HBM (c5, 160 GB, needs the host to hold A: see tests for the
+on-device-built c5 run); `--config c2` / `c4` run Alg. 4 on configs[1] / [3].
 `value` = A-stream throughput: algorithmic bytes of A streamed by the step's
 passes over A (2 for Alg. 4: the Gram pass and the A V~ pass; 2i+2 for Alg. 8)
 divided by the step time, summed over GPUs (whole job).
@@ -26,7 +29,12 @@ sys.path.insert(0, ROOT)
 
 import synth  # noqa: E402
 
-MEASURED_FP64_DMMA_TFLOPS = 37.2  # tools/fp64_peak.cu on this pool's B200 (profiles/r01_fp64_peak.txt)
+
+def fp64_peak():
+    """FP64 tensor (DMMA.8x8x4) peak measured on this pool's B200 by tools/fp64_peak.cu, committed
+    as profiles/fp64_peak.json (MEASURED_PEAKS.json, driver-written, has no FP64 entry)."""
+    d = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+    return d["dmma_tflops_sustained"], d
 
 
 def parse():
@@ -34,7 +42,7 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--config", default="c2")
+    p.add_argument("--config", default="c3")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--wp", type=float, default=1e-11)
     p.add_argument("--no-e2e", action="store_true")
@@ -98,12 +106,13 @@ PASS_KERNEL = {"xv": "gemm_nn_kernel", "qnorm": "gemm_nn_kernel", "uout": "gemm_
 
 
 def ncu_traffic(config, kind):
-    """(DRAM bytes per launch (read + write), source file) of the dominant pass's kernel, from
-    the committed ncu --set full capture of this workload (profiles/r01_<config>_ncu_full_summary.txt,
-    first matching launch in step order), or (None, None) when no capture of this workload exists."""
-    path = os.path.join(ROOT, "profiles", f"r01_{config}_ncu_full_summary.txt")
+    """(DRAM bytes per launch (read + write), source file) of a pass's kernel, from the committed
+    ncu --set full capture of this workload (profiles/r0N_<config>_ncu_full_summary.txt, newest
+    round first; first matching launch in step order), or (None, None) without a capture."""
     name = PASS_KERNEL.get(kind)
-    if not name or not os.path.exists(path):
+    paths = [os.path.join(ROOT, "profiles", f"r0{r}_{config}_ncu_full_summary.txt") for r in (2, 1)]
+    path = next((p for p in paths if os.path.exists(p)), None)
+    if not name or not path:
         return None, None
     order = ["gram_x", "xv", "gram_y", "qnorm", "uout"]  # launch order of one tssvd call
     want = [k for k in order if PASS_KERNEL.get(k) == name].index(kind) if kind in order else 0
@@ -112,13 +121,20 @@ def ncu_traffic(config, kind):
         if line.startswith(name):
             if seen == want:
                 try:
-                    rd = float(line.split("dram_rd=")[1].split("G")[0])
-                    wr = float(line.split("dram_wr=")[1].split("G")[0])
-                    return round((rd + wr) * 1e9), os.path.relpath(path, ROOT)
+                    return round((_gbytes(line, "dram_rd=") + _gbytes(line, "dram_wr=")) * 1e9), \
+                        os.path.relpath(path, ROOT)
                 except (IndexError, ValueError):
                     return None, None
             seen += 1
     return None, None
+
+
+def _gbytes(line, key):
+    v = line.split(key)[1].split()[0]
+    for unit, f in (("Gbyte", 1.0), ("Mbyte", 1e-3), ("Kbyte", 1e-6), ("byte", 1e-9)):
+        if v.endswith(unit):
+            return float(v[:-len(unit)]) * f
+    return float(v)
 
 
 def a_passes(cfg):
@@ -261,43 +277,67 @@ def run_ours(args, rank, world, local_rank):
 
     # e2e through the same C-ABI call with HOST buffers (H2D of A, D2H of U/sigma/V inside)
     e2e = None
-    if not args.no_e2e and not lowrank:
+    if not args.no_e2e:
         ts = []
-        for i in range(args.warmup + args.steps):
+        for i in range(min(args.warmup, 1) + args.steps):
             barrier()
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s0.record(stream)
-            u_h, s_h, v_h = tk.tssvd(a_host, wp=args.wp, passes=2, comm=comm)
+            if lowrank:
+                u_h, s_h, v_h = tk.lowrank_svd(a_host, om_host, cfg["iters"], cfg["k"], wp=args.wp,
+                                               comm=comm)
+            else:
+                u_h, s_h, v_h = tk.tssvd(a_host, wp=args.wp, passes=2, comm=comm)
             s1.record(stream)
             s1.synchronize()
-            if i >= args.warmup:
+            if i >= min(args.warmup, 1):
                 ts.append(s0.elapsed_time(s1))
         te = torch.tensor([statistics.mean(ts)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         r = u_h.shape[1]
+        h2d = 8 * m_local * n + (8 * om_host.numel() if lowrank else 0)
+        d2h = 8 * (m_local * r + r + n * r) if lowrank else 8 * (m_local * ((r + 1) & ~1) + r + n * r)
         e2e = {"value": round(total_a_bytes / (te.item() * 1e-3) / 1e9, 3), "unit": "GB/s",
-               "ms_per_step": round(te.item(), 3),
-               "h2d_bytes_per_step": int(8 * m_local * n),
-               "d2h_bytes_per_step": int(8 * (m_local * ((r + 1) & ~1) + r + n * r))}
+               "ms_per_step": round(te.item(), 3), "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h),
+               "path": "the same C-ABI call with pinned HOST buffers (opts.host_io = 1): H2D of A"
+                       + (" and Omega" if lowrank else "") + ", compute, D2H of U, sigma, V -- "
+                       "all inside the timed region (PCIe-bound)"}
 
-    # roofline of the dominant kernel (largest share of the step's device time)
+    # roofline of the dominant kernel (largest share of the step's device time), plus every
+    # streaming pass's own fraction; the Jacobi cores (latency-bound, no roofline) by share
+    peak, peak_info = fp64_peak()
     shares = {k: sum(v) / args.steps for k, v in pass_ms.items()}
     dom = max((k for k in shares if k != "jacobi"), key=lambda k: shares[k])
-    avg_ms = statistics.mean(pass_ms[dom])
-    flops = statistics.mean(pass_flops[dom])
-    achieved = flops / (avg_ms * 1e-3) / 1e12
+
+    def rate(kind):
+        return statistics.mean(pass_flops[kind]) / (statistics.mean(pass_ms[kind]) * 1e-3) / 1e12
+
+    achieved = rate(dom)
     traffic, traffic_src = ncu_traffic(args.config, dom)
     roof = {"kernel": dom, "bound": "tensor", "achieved": round(achieved, 3),
-            "peak": MEASURED_FP64_DMMA_TFLOPS, "unit": "TFLOP/s",
-            "frac": round(achieved / MEASURED_FP64_DMMA_TFLOPS, 4),
+            "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
             "traffic": traffic, "traffic_source": traffic_src,
             "algorithmic_bytes_per_launch": round(statistics.mean(
                 [b for k, b in zip(pass_kinds, pass_bytes) if k == dom])) if pass_bytes else None,
-            "peak_source": "FP64 DMMA.8x8x4 throughput measured on this pool's B200 by "
-                           "tools/fp64_peak.cu (MEASURED_PEAKS.json has no FP64 entry)",
+            "peak_source": "FP64 DMMA.8x8x4 sustained throughput measured on this pool's B200 by "
+                           "tools/fp64_peak.cu (profiles/fp64_peak.json; MEASURED_PEAKS.json has no "
+                           "FP64 entry)",
             "share_of_step": round(shares[dom] / t, 4),
-            "pass_ms_per_step": {k: round(v, 4) for k, v in sorted(shares.items())}}
+            "pass_ms_per_step": {k: round(v, 4) for k, v in sorted(shares.items())},
+            "pass_frac": {k: round(rate(k) / peak, 4) for k in sorted(shares) if k != "jacobi"},
+            "jacobi_share_of_step": round(shares.get("jacobi", 0.0) / t, 4)}
+
+    # Alg. 3 vs Alg. 4 orthonormality (BASELINE configs[1]): max|U^T U - I| after one and after
+    # two Gram passes, measured with a cuBLAS Gram outside the timed region
+    ortho = None
+    if not lowrank and world == 1:
+        ortho = {}
+        for npass in (1, 2):
+            u1, s1_, _ = tk.tssvd(A, wp=args.wp, passes=npass, U=U)
+            g = u1.T @ u1
+            ortho[f"pass{npass}"] = (g - torch.eye(g.shape[0], dtype=g.dtype, device=dev)).abs().max().item()
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -311,7 +351,10 @@ def run_ours(args, rank, world, local_rank):
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": ck,
                 "gpu_launches": int(launches * args.steps),
                 "kept_rank": int(out[1].numel()),
+                "ranks": st["ranks"],
                 "jacobi_sweeps": st["jacobi_sweeps"]}
+        if ortho is not None:
+            line["ortho_UtU_minus_I"] = ortho
         print(json.dumps(line), flush=True)
     if comm:
         comm.close()

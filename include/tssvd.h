@@ -16,9 +16,16 @@
  *     (pinned memory recommended) and the library stages them through the
  *     workspace with cudaMemcpyAsync on `stream`.
  *   - `stream` is a cudaStream_t (passed as void* to keep this header free of
- *     CUDA types).  All work is enqueued on it; the call synchronises the
- *     stream at the rank decisions ("Discard ..." steps) because the kept rank
- *     is returned on the host, and returns with the outputs complete.
+ *     CUDA types).  All work is enqueued on it and the call returns with the
+ *     outputs complete.  The rank decisions ("Discard ..." steps) stay on the
+ *     device: launches are sized by upper bounds and factor columns past a kept
+ *     rank are zeros, so lowrank_svd() and tssvd() with n <= 32 make ONE host
+ *     round trip (at the end, for the returned rank and the error flags).
+ *     tssvd() with n > 32 also reads back the eigensolver's count and the first
+ *     discard's rank (they size its dominant GEMMs): three round trips.
+ *   - Multi-rank: every replicated decision (kept ranks) is checked across ranks
+ *     by a max-allreduce; a rank that disagrees makes EVERY rank return
+ *     TSSVD_ENCCL instead of issuing mismatched collectives.
  *   - The caller owns every buffer (workspace included); nothing is allocated
  *     inside tssvd() / lowrank_svd().  A and Omega are never written.
  *   - Errors: every entry point returns a tssvd_status; on failure
@@ -41,7 +48,8 @@ extern "C" {
 typedef enum {
   TSSVD_OK = 0,
   TSSVD_EINVAL = 1,     /* bad argument: sizes, leading dimensions, alignment, wp, l, k, iters */
-  TSSVD_ENONFINITE = 2, /* NaN/Inf in A (or Omega), detected on the Gram diagonal */
+  TSSVD_ENONFINITE = 2, /* NaN/Inf in A (or Omega): a non-finite diagonal of the first pass's
+                           Gram matrix (also an overflowing column, |a|^2 > DBL_MAX) */
   TSSVD_ENOCONV = 3,    /* a Jacobi eigen/SVD core exceeded max_jacobi_sweeps */
   TSSVD_ECUDA = 4,      /* CUDA runtime error (detail in tssvd_last_error) */
   TSSVD_ENCCL = 5,      /* NCCL error */
@@ -97,8 +105,9 @@ void tssvd_opts_default(tssvd_opts* opts);
  * Signs: each (u_j, v_j) is flipped so the largest-|.| entry of v_j is positive.
  *
  *   m_local  rows of this rank's shard (>= 0); m = sum over ranks must be >= n
- *   n        columns, 1 <= n <= 256, n EVEN (rows move as 16-byte TMA granules)
- *   A        m_local x n, lda >= n, lda even, 16-byte aligned; read-only
+ *   n        columns, 1 <= n <= 256 (odd n allowed)
+ *   A        m_local x n, lda >= n, lda EVEN, 16-byte aligned (rows move as
+ *            16-byte TMA granules); read-only
  *   U        m_local x n capacity, ldu >= n, ldu even, 16-byte aligned: columns
  *            [0, r) receive U_p (sharded like A); the rest is scratch.
  *            U may alias A (same pointer and ldu == lda): then A is overwritten.
@@ -122,14 +131,16 @@ int tssvd(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, const doub
  * whose SVD of B = Q^T A is Algorithm 4 applied to B^T).  Returns the leading
  * k <= l triplets with ||A - U diag(sigma) V^T||_2 ~ sigma_{k+1}.
  *
- *   n        columns of A, even, n > l
+ *   n        columns of A, n > l (odd n allowed); A: lda >= n, lda EVEN, 16-byte aligned
  *   Omega    n x l start block Q~_0, ldo >= l; must be bit-identical
  *            on every rank (the caller seeds it)
  *   l, iters 0 < l < min(m, n), l <= 128; iters >= 0 (the paper's i)
  *   k        0 < k <= l
- *   U        m_local x k capacity (ldu >= k), sharded like A
+ *   U        m_local x k capacity (ldu >= k), sharded like A; device API: ldu EVEN
+ *            and U 16-byte aligned (the GEMM epilogue stores 16-byte pairs),
+ *            checked before any work is enqueued
  *   sigma    k capacity;  V  n x k capacity (ldv >= k), replicated
- *   rank     HOST out: min(k, kept rank)
+ *   rank     HOST out: min(k, kept rank); columns [rank, k) of U, V are zeros
  */
 int lowrank_workspace_size(const tssvd_comm* comm, int64_t m_local, int64_t n, int64_t l,
                            const tssvd_opts* opts, size_t* bytes);
@@ -188,13 +199,22 @@ int tssvd_matmul_tn(void* stream, int64_t m, int64_t n, int64_t l, const double*
                     size_t workspace_bytes);
 size_t tssvd_matmul_tn_workspace(int64_t m, int64_t n, int64_t l);
 /* Eigendecomposition of a symmetric POSITIVE SEMIDEFINITE B (n x n, ldb; a
- * Gram matrix) by one-sided Jacobi on its columns: lambda[j] (descending) and
- * the unit eigenvectors as ROWS of Vt (n x n, ldv): Vt[j, :] = v_j.
- * (For an indefinite B, lambda holds |eigenvalues|.) */
+ * Gram matrix; 1 <= n <= 256, else TSSVD_EINVAL) by one-sided Jacobi on its
+ * columns: lambda[j] (descending) and the unit eigenvectors as ROWS of Vt
+ * (n x n, ldv): Vt[j, :] = v_j.  (For an indefinite B, lambda holds |eigenvalues|.) */
 int tssvd_sym_eig(void* stream, int64_t n, const double* B, int64_t ldb, double* lambda,
                   double* Vt, int64_t ldv, int max_sweeps, int* sweeps, void* workspace,
                   size_t workspace_bytes);
 size_t tssvd_sym_eig_workspace(int64_t n);
+
+/* Plan-only run (no GPU, no CUDA or NCCL call): the steps and collectives that
+ * tssvd() (problem = 1; l, iters, k ignored) or lowrank_svd() (problem = 2) would
+ * take on one of `nranks` ranks holding m_local rows, written to buf as
+ * "token;token;..." (e.g. "gram:X;allreduce:gram:5050;eig:B;...").  Used by the
+ * multi-rank CPU tests, whose replay of the distributed data flow is driven by
+ * this trace of the real orchestrator.  TSSVD_ENOMEM if buf_len is too small. */
+int tssvd_trace(int problem, int nranks, int64_t m_local, int64_t n, int64_t l, int iters, int64_t k,
+                const tssvd_opts* opts, char* buf, size_t buf_len);
 
 #ifdef __cplusplus
 }

@@ -79,6 +79,8 @@ SIGNATURES = [
     ("tssvd_sym_eig", c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_int64,
                               c_int, P(c_int), c_void_p, c_size_t]),
     ("tssvd_sym_eig_workspace", c_size_t, [c_int64]),
+    ("tssvd_trace", c_int, [c_int, c_int, c_int64, c_int64, c_int64, c_int, c_int64, P(TssvdOpts),
+                            c_char_p, c_size_t]),
 ]
 
 _lock = threading.Lock()
@@ -140,6 +142,17 @@ def last_stats() -> dict:
     return dict(kernel_launches=s.kernel_launches, a_passes=s.a_passes,
                 jacobi_sweeps=list(s.jacobi_sweeps[: s.n_jacobi]),
                 ranks=list(s.ranks[: s.n_ranks]), passes=passes)
+
+
+def trace(problem: str, nranks: int, m_local: int, n: int, l: int = 0, iters: int = 0, k: int = 0,
+          wp: float = 1e-11, passes: int = 2) -> list[str]:
+    """Steps and collectives of one tssvd ('tssvd') / lowrank_svd ('lowrank') call on one of
+    `nranks` ranks, from a plan-only run of the real orchestrator (no GPU needed)."""
+    opts = default_opts(wp, passes)
+    buf = ctypes.create_string_buffer(1 << 16)
+    check(lib().tssvd_trace(1 if problem == "tssvd" else 2, nranks, m_local, n, l, iters, k,
+                            ctypes.byref(opts), buf, len(buf)))
+    return [t for t in buf.value.decode().split(";") if t]
 
 
 def set_pass_timing(enable: bool) -> None:

@@ -118,9 +118,10 @@ def tssvd(A: torch.Tensor, wp: float = 1e-11, passes: int = 2, comm: Comm | None
     ws = _workspace(nbytes.value, dev)
     pin = host and torch.cuda.is_available()
     packed = host and U is None  # host_io: U comes back packed (ld (r+1)&~1), one D2H copy
-    if U is None:
-        U = A if (inplace and not host) else torch.empty((m, n), dtype=torch.float64,
-                                                         device=A.device, pin_memory=pin)
+    if U is None:  # device API: even leading dimension (16-byte rows), also for odd n
+        U = A if (inplace and not host) else torch.empty((m, n + (n & (0 if host else 1))),
+                                                         dtype=torch.float64, device=A.device,
+                                                         pin_memory=pin)
     sigma = torch.empty(n, dtype=torch.float64, device=A.device, pin_memory=pin)
     V = torch.empty((n, n), dtype=torch.float64, device=A.device, pin_memory=pin)
     r = ctypes.c_int64()

@@ -32,6 +32,11 @@ using namespace tsk;
 thread_local std::string g_err;
 thread_local tssvd_stats g_stats;
 thread_local bool g_timing = false;
+// Plan-only ("dry") run, tssvd_trace(): no CUDA or NCCL call is made, every step the
+// orchestrator takes is appended to g_trace instead ("token;token;...").  The gloo
+// replay test drives its numpy re-enactment of the multi-rank data flow with it.
+thread_local bool g_dry = false;
+thread_local std::string g_trace;
 
 struct Fail {
   int code;
@@ -58,17 +63,35 @@ struct Fail {
     ncclResult_t e_ = (x);                                                                     \
     if (e_ != ncclSuccess) fail(TSSVD_ENCCL, "%s: %s", #x, ncclGetErrorString(e_));            \
   } while (0)
+// CUDA runtime calls of the orchestrator (copies, syncs): skipped in a dry run
+#define CUR(x)                                                                                 \
+  do {                                                                                         \
+    if (!g_dry) CU(x);                                                                         \
+  } while (0)
 #define KL(x)                                                                                  \
   do {                                                                                         \
-    CU(x);                                                                                     \
+    if (!g_dry) CU(x);                                                                         \
     ++g_stats.kernel_launches;                                                                 \
   } while (0)
 #define KS(x)                                                                                  \
   do {                                                                                         \
-    x;                                                                                         \
-    CU(cudaGetLastError());                                                                    \
+    if (!g_dry) {                                                                              \
+      x;                                                                                       \
+      CU(cudaGetLastError());                                                                  \
+    }                                                                                          \
     ++g_stats.kernel_launches;                                                                 \
   } while (0)
+
+void step(const char* fmt, ...) {
+  if (!g_dry) return;
+  char buf[128];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_trace += buf;
+  g_trace += ';';
+}
 
 template <class F>
 int guarded(F&& f) {
@@ -99,39 +122,48 @@ struct Arena {
   }
 };
 
-int* pinned_ints() {
-  static thread_local int* p = nullptr;
-  if (!p) CU(cudaHostAlloc(reinterpret_cast<void**>(&p), 16 * sizeof(int), cudaHostAllocDefault));
-  return p;
-}
+// Per-call control block in device memory, read back once at the end of the call:
+//   jinfo : deferred Jacobi solves, 8 ints each {sweeps, converged, k, -, -, rounds, nonfinite, -}
+//   slots : "Discard" decisions, 8 ints each (small_kernels.h kSlot*)
+//   guard : multi-rank: max-allreduced copy of the slots (every rank must match it)
+//   m64   : multi-rank: global row count (int64 allreduce), validated at the end
+constexpr int kMaxDeferred = 48, kMaxSlots = 32;
+constexpr int kCtlInts = 8 * kMaxDeferred + 2 * 8 * kMaxSlots + 4;
 
 struct Ctx {
   tssvd_comm* comm = nullptr;
   cudaStream_t s = nullptr;
   double wp = 1e-11;
   int max_sweeps = 60;
-  // Jacobi solves whose convergence is checked after the call's final sync
-  // (no host round trip per solve): device info slots of 8 ints each
-  int* jinfo = nullptr;
-  int njinfo = 0;
-  static constexpr int kMaxDeferred = 48;
+  int* ctl = nullptr;  // device, kCtlInts
+  int njinfo = 0, nslots = 0;
   bool dist() const { return comm && comm->nranks > 1; }
+  int* jinfo() const { return ctl; }
+  int* slots() const { return ctl + 8 * kMaxDeferred; }
+  int* guard() const { return ctl + 8 * kMaxDeferred + 8 * kMaxSlots; }
+  int64_t* m64() const { return reinterpret_cast<int64_t*>(ctl + 8 * kMaxDeferred + 16 * kMaxSlots); }
   int* next_info() {
     if (njinfo >= kMaxDeferred) fail(TSSVD_ECUDA, "too many deferred Jacobi solves");
-    return jinfo + 8 * njinfo++;
+    return jinfo() + 8 * njinfo++;
   }
+  int next_slot() {
+    if (nslots >= kMaxSlots) fail(TSSVD_ECUDA, "too many discard decisions");
+    return nslots++;
+  }
+  int* slot(int i) const { return slots() + 8 * i; }
 };
 
-void allreduce(Ctx& c, double* buf, int64_t count) {
-  if (!c.dist() || count <= 0) return;
-  NC(ncclAllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, c.comm->nccl, c.s));
+// pinned host mirror of the control block
+int* host_ctl() {
+  static thread_local int* p = nullptr;
+  if (!p) CU(cudaHostAlloc(reinterpret_cast<void**>(&p), (kCtlInts + 4) * sizeof(int), cudaHostAllocDefault));
+  return p;
 }
 
-void read_ints(Ctx& c, const int* dev, int n, int* host) {
-  int* h = pinned_ints();
-  CU(cudaMemcpyAsync(h, dev, n * sizeof(int), cudaMemcpyDeviceToHost, c.s));
-  CU(cudaStreamSynchronize(c.s));
-  std::memcpy(host, h, n * sizeof(int));
+void allreduce(Ctx& c, double* buf, int64_t count, const char* what) {
+  if (!c.dist() || count <= 0) return;
+  step("allreduce:%s:%lld", what, (long long)count);
+  if (!g_dry) NC(ncclAllReduce(buf, buf, (size_t)count, ncclDouble, ncclSum, c.comm->nccl, c.s));
 }
 
 // Per-pass CUDA-event timing (tssvd_set_pass_timing): events recorded on the
@@ -141,7 +173,7 @@ struct PassTimer {
   int open = -1;
   cudaStream_t s = nullptr;
   void begin(cudaStream_t st, int kind, double flops, double bytes) {
-    if (!g_timing || g_stats.n_pass >= TSSVD_MAX_PASSES) return;
+    if (g_dry || !g_timing || g_stats.n_pass >= TSSVD_MAX_PASSES) return;
     const int i = g_stats.n_pass;
     for (int q = 0; q < 2; ++q)
       if (!ev[2 * i + q]) CU(cudaEventCreate(&ev[2 * i + q]));
@@ -159,6 +191,7 @@ struct PassTimer {
     open = -1;
   }
   void resolve() {
+    if (g_dry) return;
     for (int i = 0; i < g_stats.n_pass; ++i) {
       float ms = 0.f;
       CU(cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]));
@@ -180,8 +213,8 @@ inline int mrows_for(int k) { return (int)(gemm_nn_m_doubles(k, 1) / smem_ld(1))
 struct Core {
   int64_t m_local = 0;
   int w = 0;
-  double *part, *npart, *B, *lam, *nsq, *sig, *M, *G, *Z, *dz, *tsq, *T, *Rt, *sv, *Ps;
-  int *idx, *idx2, *iout, *info;
+  double *part, *npart, *B, *Bp, *lam, *nsq, *sig, *M, *G, *Z, *dz, *tsq, *T, *Rt, *sv, *Ps;
+  int *idx, *idx2, *info;
   void alloc(Arena& a, int64_t m, int ww) {
     m_local = m;
     w = ww;
@@ -193,6 +226,7 @@ struct Core {
       nn = std::max(nn, (size_t)gemm_nn_grid(std::max<int64_t>(m, 1), q) * gemm_nn_part_stride(q));
     npart = a.get<double>(nn);
     B = a.get<double>((size_t)w * w);
+    Bp = a.get<double>((size_t)w * (w + 1) / 2);
     lam = a.get<double>(w);
     nsq = a.get<double>(w);
     sig = a.get<double>(w);
@@ -207,30 +241,90 @@ struct Core {
     Ps = a.get<double>((size_t)w * w);
     idx = a.get<int>(w);
     idx2 = a.get<int>(w);
-    iout = a.get<int>(8);
     info = a.get<int>(8);
   }
 };
 
-int jacobi_info(Ctx& c, const int* info, const char* what, int N) {
-  int h[3];
-  read_ints(c, info, 3, h);
-  if (g_stats.n_jacobi < 16) g_stats.jacobi_sweeps[g_stats.n_jacobi++] = h[0];
-  if (!h[1]) fail(TSSVD_ENOCONV, "Jacobi %s (N=%d) not converged in %d sweeps", what, N, h[0]);
-  return h[2];
+// Host-side counters of a finished call: sweeps of every Jacobi solve, kept ranks.
+void note_rank(int64_t r) {
+  if (g_stats.n_ranks < 8) g_stats.ranks[g_stats.n_ranks++] = r;
 }
 
-// After the final sync of a call: every deferred solve must have converged.
-void check_deferred(Ctx& c) {
-  if (!c.njinfo) return;
-  static thread_local int* h = nullptr;
-  if (!h) CU(cudaHostAlloc(reinterpret_cast<void**>(&h), 8 * Ctx::kMaxDeferred * sizeof(int), cudaHostAllocDefault));
-  CU(cudaMemcpyAsync(h, c.jinfo, 8 * c.njinfo * sizeof(int), cudaMemcpyDeviceToHost, c.s));
-  CU(cudaStreamSynchronize(c.s));
-  for (int q = 0; q < c.njinfo; ++q) {
-    if (g_stats.n_jacobi < 16) g_stats.jacobi_sweeps[g_stats.n_jacobi++] = h[8 * q];
-    if (!h[8 * q + 1]) fail(TSSVD_ENOCONV, "Jacobi solve %d not converged in %d sweeps", q, h[8 * q]);
+// Reads n ints at dev into host (one round trip; dry run: `dry_val` everywhere).
+void read_ints(Ctx& c, const int* dev, int n, int* host, int dry_val) {
+  if (g_dry) {
+    for (int i = 0; i < n; ++i) host[i] = dry_val;
+    return;
   }
+  int* h = host_ctl();
+  CU(cudaMemcpyAsync(h, dev, n * sizeof(int), cudaMemcpyDeviceToHost, c.s));
+  CU(cudaStreamSynchronize(c.s));
+  std::memcpy(host, h, n * sizeof(int));
+}
+
+// Host-mode decision: the discard's slot is read now (its r sizes the next launches).
+// Multi-rank: max-allreduce of the guard words first, in the same round trip -- a rank
+// whose r or nc differs from another's fails on EVERY rank instead of issuing a
+// differently sized collective (a hang).
+void decide_now(Ctx& c, int slot, int* r, int* nc, int bound, const char* what) {
+  step("sync:%s", what);
+  int* sl = c.slot(slot);
+  if (g_dry) {
+    *r = *nc = bound;
+    return;
+  }
+  int* gw = c.guard() + 8 * slot;
+  if (c.dist()) {
+    CU(cudaMemcpyAsync(gw, sl + kSlotGuard, 4 * sizeof(int), cudaMemcpyDeviceToDevice, c.s));
+    NC(ncclAllReduce(gw, gw, 4, ncclInt32, ncclMax, c.comm->nccl, c.s));
+  }
+  int* h = host_ctl();
+  CU(cudaMemcpyAsync(h, sl, 8 * sizeof(int), cudaMemcpyDeviceToHost, c.s));
+  if (c.dist()) CU(cudaMemcpyAsync(h + 8, gw, 4 * sizeof(int), cudaMemcpyDeviceToHost, c.s));
+  CU(cudaStreamSynchronize(c.s));
+  if (c.dist() && (h[8] != h[kSlotGuard] || h[9] != h[kSlotGuard + 1] || h[10] != h[kSlotGuard + 2] ||
+                   h[11] != h[kSlotGuard + 3]))
+    fail(TSSVD_ENCCL, "replicated discard decision (%s) differs across ranks (r %d vs max %d)", what, h[0], h[8]);
+  if (h[kSlotBad]) fail(TSSVD_ENONFINITE, "non-finite entries in the input (%s)", what);
+  *r = h[kSlotR];
+  *nc = h[kSlotNc];
+}
+
+// End of a call: ONE round trip reads the whole control block (deferred Jacobi
+// convergence, device-side decisions, the multi-rank guard and global m).
+struct Finish {
+  int jinfo[8 * kMaxDeferred];
+  int slots[8 * kMaxSlots];
+  int64_t m = -1;
+};
+void finish(Ctx& c, Finish& f) {
+  step("finish");
+  if (g_dry) {
+    for (int q = 0; q < c.nslots; ++q) f.slots[8 * q] = f.slots[8 * q + 1] = 1 << 20;
+    return;
+  }
+  if (c.dist() && c.nslots > 0) {
+    CU(cudaMemcpyAsync(c.guard(), c.slots(), 8 * c.nslots * sizeof(int), cudaMemcpyDeviceToDevice, c.s));
+    NC(ncclAllReduce(c.guard(), c.guard(), 8 * c.nslots, ncclInt32, ncclMax, c.comm->nccl, c.s));
+  }
+  int* h = host_ctl();
+  CU(cudaMemcpyAsync(h, c.ctl, kCtlInts * sizeof(int), cudaMemcpyDeviceToHost, c.s));
+  CU(cudaStreamSynchronize(c.s));
+  std::memcpy(f.jinfo, h, sizeof f.jinfo);
+  std::memcpy(f.slots, h + 8 * kMaxDeferred, sizeof f.slots);
+  const int* g = h + 8 * kMaxDeferred + 8 * kMaxSlots;
+  std::memcpy(&f.m, h + 8 * kMaxDeferred + 16 * kMaxSlots, sizeof(int64_t));
+  for (int q = 0; q < c.njinfo; ++q)
+    if (g_stats.n_jacobi < 16) g_stats.jacobi_sweeps[g_stats.n_jacobi++] = f.jinfo[8 * q];
+  for (int q = 0; q < c.nslots; ++q) note_rank(f.slots[8 * q + kSlotR]);
+  if (c.dist())
+    for (int q = 0; q < 8 * c.nslots; ++q)
+      if (g[q] != f.slots[q])
+        fail(TSSVD_ENCCL, "replicated discard decision %d differs across ranks", q / 8);
+  for (int q = 0; q < c.nslots; ++q)
+    if (f.slots[8 * q + kSlotBad]) fail(TSSVD_ENONFINITE, "non-finite entries in the input (A or Omega)");
+  for (int q = 0; q < c.njinfo; ++q)
+    if (!f.jinfo[8 * q + 1]) fail(TSSVD_ENOCONV, "Jacobi solve %d not converged in %d sweeps", q, f.jinfo[8 * q]);
 }
 
 // One-sided Jacobi rotation threshold for columns of `rows` dot-product rows:
@@ -239,58 +333,87 @@ void check_deferred(Ctx& c) {
 // n eps threshold let the orthonormality of U drift to 1.1e-13 at r = 128).
 inline double jacobi_tol(int rows) { return std::max(8.0, 2.0 * std::sqrt((double)rows)) * kEps; }
 
-// Eigendecomposition of the PSD matrix B (n x n, ld n) in place: returns k and
-// leaves eigenvector j (unit, descending eigenvalue) at B + j*n.  Pivots below
-// trunc_rel * max diag are dropped (numerically null directions; reading R10).
-// sync = false: no host round trip -- returns n (the kernel zero-fills the
-// eigenvector slots [k, n), which then carry zero norms into the next discard)
-// and convergence is checked after the call.
-int eig(Ctx& c, Core& b, double* B, int n, double* vals, double trunc_rel, bool sync = true) {
-  Pass t(c.s, TSSVD_PASS_JACOBI, 0, 0);
+// Eigendecomposition of the PSD matrix B (n x n, ld n) in place: eigenvector j
+// (unit, descending eigenvalue) at B + j*n; slots past the solver's k are zero.
+// Pivots below trunc_rel * max diag are dropped (numerically null directions;
+// reading R13).  sync = true: one round trip returns k (it sizes the next GEMM);
+// sync = false: returns the bound n, convergence is checked at the end of the call.
+// *nf_flag receives the device address of the solve's non-finite flag.
+int eig(Ctx& c, Core& b, double* B, int n, double* vals, double trunc_rel, bool sync, const int** nf_flag,
+        const char* what) {
+  step("eig:%s", what);
   int* info = sync ? b.info : c.next_info();
-  KL(launch_jacobi_eig(B, n, n, jacobi_tol(n), trunc_rel, c.max_sweeps, B, n, vals, info, c.s));
-  return sync ? jacobi_info(c, info, "eig", n) : n;
+  {
+    Pass t(c.s, TSSVD_PASS_JACOBI, 0, 0);
+    KL(launch_jacobi_eig(B, n, n, jacobi_tol(n), trunc_rel, c.max_sweeps, B, n, vals, info, c.s));
+  }
+  *nf_flag = info + 6;
+  if (!sync) return n;
+  step("sync:k_%s", what);
+  int h[7];
+  read_ints(c, info, 7, h, n);
+  if (g_dry) return n;
+  if (g_stats.n_jacobi < 16) g_stats.jacobi_sweeps[g_stats.n_jacobi++] = h[0];
+  if (h[6]) fail(TSSVD_ENONFINITE, "non-finite entries in the input (Gram diagonal)");
+  if (!h[1]) fail(TSSVD_ENOCONV, "Jacobi eig (N=%d) not converged in %d sweeps", n, h[0]);
+  return h[2];
 }
 
-void note_rank(int64_t r) {
-  if (g_stats.n_ranks < 8) g_stats.ranks[g_stats.n_ranks++] = r;
-}
+// Result of one Alg. 3/4 run: `bound` columns were written (host shape); the kept
+// rank itself is slot(slot)[kSlotR] (known on the host only after finish(), unless
+// exact).  The factor columns [rank, bound) are zeros.
+struct CoreOut {
+  int bound = 0;
+  int slot = -1;
+  bool exact = false;
+};
 
 // Alg. 3 (passes = 1) or Alg. 4 (passes = 2) on X
 // (m_local x w, ldx; row-sharded over the communicator when dist, replicated
 // otherwise).  U (m_local x w capacity, ldu) receives U[:, :r]; may alias X.
-// sigma[:r], V (w x r, ldv) replicated.  Returns r.
-int64_t core(Ctx& c, Core& b, const double* X, int64_t ldx, int64_t m_local, int w, int passes,
-             bool dist, double* U, int64_t ldu, double* sigma, double* V, int64_t ldv,
+// sigma[:r], V (w x r, ldv) replicated.
+// devmode: every rank decision stays on the device (shapes sized by the bound w,
+// zero columns past the device count; no host round trip at all).  Otherwise
+// the eigensolver's k and the first discard's r are read back (they size the
+// dominant GEMMs of a wide core); the second discard always stays on the device.
+CoreOut core(Ctx& c, Core& b, const double* X, int64_t ldx, int64_t m_local, int w, int passes, bool dist,
+             double* U, int64_t ldu, double* sigma, double* V, int64_t ldv, bool devmode,
              double* Upack = nullptr) {
-  // Upack: the final U is written there packed, leading dimension (r + 1) & ~1, instead of in place
+  // Upack: the final U is written there packed (leading dimension (bound + 1) & ~1)
   cudaStream_t s = c.s;
   Ctx cd = c;
   if (!dist) cd.comm = nullptr;
+  const bool dd = cd.dist();
+  step("core:%s:%d:%d", dist ? "sharded" : "local", passes, w);
   // truncation of the eigensolver's pivoted Cholesky (reading R13): directions with
   // lambda <= 0.01 wp lambda_max have Sigma~^2 <= lambda + |E| far below the discard line
   // wp Sigma~_max^2, so they could never be kept; the truncated Schur complement
   // (<= (n-K) trunc lambda_max) moves the kept sigma by ~1e-13 sigma_1 (simulated at c2/c4),
   // three orders below the 1e-10 contract.
   const double trunc = std::max(kEps, 0.01 * c.wp);
-  // Step 1 (P:613 / P:646): B = A^* A over the local rows, aggregated across ranks.
+  // Step 1 (P:613 / P:646): B = A^* A over the local rows, aggregated across ranks
+  // (the packed lower triangle: w(w+1)/2 doubles on the wire).
+  step("gram:X");
   {
     Pass t(s, TSSVD_PASS_GRAM_X, (double)m_local * w * (w + 1), 8.0 * m_local * w);
     KL(launch_syrk(X, ldx, m_local, w, b.part, s));
-    KL(launch_reduce_sym(b.part, syrk_partials_grid(m_local, w), w, b.B, w, s));
+    KL(launch_reduce_sym(b.part, syrk_partials_grid(m_local, w), w, b.B, w, dd ? b.Bp : nullptr, s));
   }
-  if (cd.dist()) {
-    allreduce(cd, b.B, (int64_t)w * w);
-    KS(symmetrize(b.B, w, w, s));
+  if (dd) {
+    allreduce(cd, b.Bp, (int64_t)w * (w + 1) / 2, "gram");
+    KS(unpack_sym(b.Bp, w, b.B, w, s));
   }
   // Step 2 (P:615 / P:648): B = V~ D V~^*  -> k eigenvectors (columns of B's buffer).
-  const int k = eig(c, b, b.B, w, b.lam, trunc);
-  if (k == 0) {  // B == 0 (or non-finite): nothing survives
-    note_rank(0);
-    return 0;
+  const int* nf = nullptr;
+  const int k = eig(c, b, b.B, w, b.lam, trunc, !devmode, &nf, "B");
+  CoreOut out;
+  if (k == 0) {  // host mode, B == 0: nothing survives (device mode carries zeros instead)
+    out.exact = true;
+    return out;
   }
   // Step 3 (P:619 / P:652): Y~ = A V~ (k columns) written into U;
   // Step 4 (P:621 / P:654): Sigma~ = column norms (sums of squares fused, then reduced).
+  step("xv:%d", k);
   KS(cols_to_m(b.B, w, w, k, b.M, smem_ld(k), mrows_for(w), s));
   {
     Pass t(s, TSSVD_PASS_XV, 2.0 * m_local * w * k, 8.0 * m_local * (w + k));
@@ -298,77 +421,103 @@ int64_t core(Ctx& c, Core& b, const double* X, int64_t ldx, int64_t m_local, int
     KL(launch_reduce_parts(b.npart, gemm_nn_grid(std::max<int64_t>(m_local, 1), k), gemm_nn_part_stride(k), k, b.nsq, s));
   }
   ++g_stats.a_passes;
-  allreduce(cd, b.nsq, k);
+  allreduce(cd, b.nsq, k, "norms");
   // Step 5 (P:625 / P:658): discard below max * sqrt(wp).
-  KS(discard(b.nsq, k, c.wp, b.sig, b.idx, b.iout, nullptr, 0, s));
-  int h[3];
-  read_ints(c, b.iout, 3, h);
-  if (h[2]) fail(TSSVD_ENONFINITE, "non-finite entries in the input (column norms)");
-  const int r = h[0], nc = h[1];
-  note_rank(r);
-  if (r == 0) return 0;
+  step("discard:1");
+  const int s1 = c.next_slot();
+  int* d1 = c.slot(s1);
+  KS(discard(b.nsq, k, c.wp, b.sig, b.idx, d1, nf, s));
+  int r = k, nc = k;  // device mode: shape bounds
+  if (!devmode) {
+    decide_now(c, s1, &r, &nc, k, "first discard");
+    if (r == 0) {
+      out.slot = s1;
+      out.exact = true;
+      return out;
+    }
+  }
 
   if (passes == 1) {
     // Step 6: U = Y~ Sigma^-1 (kept columns, sorted by Sigma, signs fixed), in place.
+    step("alg3_out");
     const int ldm = smem_ld(r);
     KS(fill(b.M, (int64_t)mrows_for(nc) * ldm, 0.0, s));
-    KS(alg3_out(b.sig, b.idx, r, b.B, w, b.M, ldm, sigma, V, ldv, s));
+    KS(alg3_out(b.sig, b.idx, d1, r, b.B, w, b.M, ldm, sigma, V, ldv, s));
+    step("uout:%d", r);
     {
       Pass t(s, TSSVD_PASS_UOUT, 2.0 * m_local * nc * r, 8.0 * m_local * (nc + r));
       KL(launch_gemm_nn(U, ldu, m_local, nc, b.M, r, Upack ? Upack : U, Upack ? (r + 1) & ~1 : ldu,
                         nullptr, s));
     }
-    return r;
+    out.bound = r;
+    out.slot = s1;
+    out.exact = !devmode;
+    return out;
   }
   // Steps 6-7: Z = Y^* Y = Sigma~^-1 (Y~^* Y~)_keep Sigma~^-1.
+  step("gram:Y:%d", nc);
   {
     Pass t(s, TSSVD_PASS_GRAM_Y, (double)m_local * nc * (nc + 1), 8.0 * m_local * nc);
     KL(launch_syrk(U, ldu, m_local, nc, b.part, s));
-    KL(launch_reduce_sym(b.part, syrk_partials_grid(m_local, nc), nc, b.G, nc, s));
+    KL(launch_reduce_sym(b.part, syrk_partials_grid(m_local, nc), nc, b.G, nc, dd ? b.Bp : nullptr, s));
   }
-  if (cd.dist()) {
-    allreduce(cd, b.G, (int64_t)nc * nc);
-    KS(symmetrize(b.G, nc, nc, s));
+  if (dd) {
+    allreduce(cd, b.Bp, (int64_t)nc * (nc + 1) / 2, "gram");
+    KS(unpack_sym(b.Bp, nc, b.G, nc, s));
   }
-  KS(build_z(b.G, nc, b.idx, b.sig, r, b.Z, s));
-  // Step 8: Z = W D W^*  (W: r x kz, column-major in b.Z).
-  const int kz = eig(c, b, b.Z, r, b.dz, trunc, false);  // Z = Y^T Y ~ I: kz = r
+  const int rb = r;  // bound of r (exact in host mode)
+  step("build_z");
+  KS(build_z(b.G, nc, b.idx, b.sig, d1, rb, b.Z, s));
+  // Step 8: Z = W D W^*  (W: rb x kz, column-major in b.Z).
+  const int* nfz = nullptr;
+  const int kz = eig(c, b, b.Z, rb, b.dz, trunc, false, &nfz, "Z");  // Z = Y^T Y ~ I: kz = r
   // Steps 9-10: Q~ = Y W, T = column norms of Q~ (norms only, nothing stored).
+  step("qnorm:%d", kz);
   const int ldm_k = smem_ld(kz);
   KS(fill(b.M, (int64_t)mrows_for(nc) * ldm_k, 0.0, s));
-  KS(build_m1(b.Z, b.idx, b.sig, r, kz, b.M, ldm_k, s));
+  KS(build_m1(b.Z, rb, b.idx, b.sig, d1, rb, kz, b.M, ldm_k, s));
   {
     Pass t(s, TSSVD_PASS_QNORM, 2.0 * m_local * nc * kz, 8.0 * m_local * nc);
     KL(launch_gemm_nn(U, ldu, m_local, nc, b.M, kz, nullptr, 0, b.npart, s));
     KL(launch_reduce_parts(b.npart, gemm_nn_grid(std::max<int64_t>(m_local, 1), kz), gemm_nn_part_stride(kz), kz, b.tsq, s));
   }
-  allreduce(cd, b.tsq, kz);
-  // Step 11: discard T below max(T) sqrt(wp).
-  KS(discard(b.tsq, kz, c.wp, b.T, b.idx2, b.iout, nullptr, 0, s));
-  read_ints(c, b.iout, 3, h);
-  if (h[2]) fail(TSSVD_ENONFINITE, "non-finite column norms in the second orthonormalization");
-  const int r2 = h[0];
-  note_rank(r2);
-  if (r2 == 0) return 0;
+  allreduce(cd, b.tsq, kz, "norms");
+  // Step 11: discard T below max(T) sqrt(wp) -- r2 stays on the device: every
+  // later launch is sized by its bound rb2 = kz (= r, as Z ~ I keeps every direction).
+  step("discard:2");
+  const int s2 = c.next_slot();
+  int* d2 = c.slot(s2);
+  KS(discard(b.tsq, kz, c.wp, b.T, b.idx2, d2, nfz, s));
+  const int rb2 = kz;
   // Steps 12-14: R = T W^* Sigma~ V~^* = K V~_keep^T with K = T W_keep^T Sigma~
   // (r2 x r); SVD of K by one-sided Jacobi on its columns, K J = P Sigma  =>  V = V~_keep J.
-  KS(build_k(b.T, b.idx2, r2, b.Z, r, b.sig, b.idx, b.Rt, s));
+  step("svd:R");
+  KS(build_k(b.T, b.idx2, d2, rb2, b.Z, rb, d1, rb, b.sig, b.idx, b.Rt, s));
   {
     Pass t(s, TSSVD_PASS_JACOBI, 0, 0);
-    KL(launch_jacobi_svd(b.Rt, r2, r, r2, jacobi_tol(r2), c.max_sweeps, b.Rt + (size_t)r2 * r,
-                         r2 + r, b.sv, c.next_info(), s));
+    KL(launch_jacobi_svd(b.Rt, rb2, rb, rb2, jacobi_tol(rb2), c.max_sweeps, b.Rt + (size_t)rb2 * rb,
+                         rb2 + rb, b.sv, c.next_info(), s));
   }
-  KS(svd_out(b.Rt + (size_t)r2 * r, r2 + r, r2, r, b.sv, b.B, w, b.idx, sigma, V, ldv, b.Ps, s));
+  KS(svd_out(b.Rt + (size_t)rb2 * rb, rb2 + rb, d2, rb2, d1, b.sv, b.B, w, b.idx, sigma, V, ldv, b.Ps, s));
   // Step 15: U = Q P = Y~[:, :nc] (S W T^-1 P), in place.
-  const int ldm_r2 = smem_ld(r2);
+  step("uout:%d", rb2);
+  const int ldm_r2 = smem_ld(rb2);
   KS(fill(b.M, (int64_t)mrows_for(nc) * ldm_r2, 0.0, s));
-  KS(build_m2(b.Z, r, b.idx, b.sig, b.T, b.idx2, r2, b.Ps, b.M, ldm_r2, s));
+  KS(build_m2(b.Z, rb, d1, rb, b.idx, b.sig, b.T, b.idx2, d2, rb2, b.Ps, b.M, ldm_r2, s));
   {
-    Pass t(s, TSSVD_PASS_UOUT, 2.0 * m_local * nc * r2, 8.0 * m_local * (nc + r2));
-    KL(launch_gemm_nn(U, ldu, m_local, nc, b.M, r2, Upack ? Upack : U, Upack ? (r2 + 1) & ~1 : ldu,
+    Pass t(s, TSSVD_PASS_UOUT, 2.0 * m_local * nc * rb2, 8.0 * m_local * (nc + rb2));
+    KL(launch_gemm_nn(U, ldu, m_local, nc, b.M, rb2, Upack ? Upack : U, Upack ? (rb2 + 1) & ~1 : ldu,
                       nullptr, s));
   }
-  return r2;
+  out.bound = rb2;
+  out.slot = s2;
+  return out;
+}
+
+// kept rank of a finished core
+int64_t core_rank(const CoreOut& o, const Finish& f) {
+  if (o.slot < 0) return 0;
+  return f.slots[8 * o.slot + kSlotR];
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -383,50 +532,60 @@ void check_opts(const tssvd_opts* o) {
 }
 
 void set_device(tssvd_comm* comm) {
-  if (comm) CU(cudaSetDevice(comm->device));
+  if (comm && !g_dry) CU(cudaSetDevice(comm->device));
 }
 
-// global m = sum of m_local over ranks (int64 allreduce), used for validation
-int64_t global_rows(Ctx& c, int64_t m_local, void* scratch_dev) {
+// Global m = sum of m_local over ranks: an int64 allreduce on the device, validated
+// in finish() (single rank: known now).  Returns m when known now, else -1.
+int64_t global_rows(Ctx& c, int64_t m_local) {
   if (!c.dist()) return m_local;
-  int64_t* d = static_cast<int64_t*>(scratch_dev);
-  int64_t* h = reinterpret_cast<int64_t*>(pinned_ints());
+  step("allreduce:m:1");
+  if (g_dry) return -1;
+  int64_t* h = reinterpret_cast<int64_t*>(host_ctl() + kCtlInts);  // own staging word (H2D in flight)
   *h = m_local;
-  CU(cudaMemcpyAsync(d, h, 8, cudaMemcpyHostToDevice, c.s));
-  NC(ncclAllReduce(d, d, 1, ncclInt64, ncclSum, c.comm->nccl, c.s));
-  CU(cudaMemcpyAsync(h, d, 8, cudaMemcpyDeviceToHost, c.s));
-  CU(cudaStreamSynchronize(c.s));
-  return *h;
+  CU(cudaMemcpyAsync(c.m64(), h, 8, cudaMemcpyHostToDevice, c.s));
+  NC(ncclAllReduce(c.m64(), c.m64(), 1, ncclInt64, ncclSum, c.comm->nccl, c.s));
+  return -1;
+}
+
+// Device-side rank decisions for a tall-skinny core of width w: always for narrow
+// cores (bound-sized launches cost nothing there); wide cores read k and r back
+// because they size the dominant GEMMs.  TSSVD_DEVICE_RANK=1/0 forces (experiments).
+bool devmode_for(int w) {
+  static const int force = getenv("TSSVD_DEVICE_RANK") ? atoi(getenv("TSSVD_DEVICE_RANK")) : -1;
+  if (force >= 0) return force != 0;
+  return w <= 32;
 }
 
 struct TsPlan {
   Core core;
-  int* jinfo;
-  int64_t* m_scratch;
+  int* ctl;
   double* a_stage;  // host_io: device copy of A (also holds Y~)
   double* u_pack;   // host_io: U packed (ld (r+1)&~1) for one contiguous D2H copy
   double* sig_stage;
   double* v_stage;
 };
 
+inline int64_t even(int64_t x) { return (x + 1) & ~int64_t(1); }
+
 size_t plan_tssvd(Arena& a, TsPlan& p, int64_t m_local, int n, const tssvd_opts* o) {
-  p.jinfo = a.get<int>(8 * Ctx::kMaxDeferred);
-  p.m_scratch = a.get<int64_t>(2);
+  p.ctl = a.get<int>(kCtlInts);
   p.core.alloc(a, m_local, n);
   if (o && o->host_io) {
-    p.a_stage = a.get<double>((size_t)std::max<int64_t>(m_local, 1) * n);
-    p.u_pack = a.get<double>((size_t)std::max<int64_t>(m_local, 1) * ((n + 1) & ~1));
+    p.a_stage = a.get<double>((size_t)std::max<int64_t>(m_local, 1) * even(n));
+    p.u_pack = a.get<double>((size_t)std::max<int64_t>(m_local, 1) * even(n));
     p.sig_stage = a.get<double>(n);
     p.v_stage = a.get<double>((size_t)n * n);
   }
   return a.off;
 }
 
-void validate_tall(int64_t m_local, int64_t n, int64_t lda) {
+// host_io: A is staged with an even leading dimension, so any lda >= n is accepted
+void validate_tall(int64_t m_local, int64_t n, int64_t lda, bool hio) {
   if (m_local < 0) fail(TSSVD_EINVAL, "m_local < 0");
   if (n < 1 || n > 256) fail(TSSVD_EINVAL, "n = %lld must be in [1, 256]", (long long)n);
-  if (n & 1) fail(TSSVD_EINVAL, "n = %lld must be even (rows move as 16-byte TMA granules)", (long long)n);
-  if (lda < n || (lda & 1)) fail(TSSVD_EINVAL, "lda = %lld must be even and >= n", (long long)lda);
+  if (lda < n || (!hio && (lda & 1)))
+    fail(TSSVD_EINVAL, "lda = %lld must be even and >= n (16-byte TMA row strides)", (long long)lda);
 }
 
 void tssvd_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, const double* A,
@@ -434,7 +593,7 @@ void tssvd_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, cons
                 double* V, int64_t ldv, int64_t* rank, void* ws, size_t ws_bytes) {
   g_stats = tssvd_stats{};
   check_opts(opts);
-  validate_tall(m_local, n, lda);
+  validate_tall(m_local, n, lda, opts->host_io == 1);
   if (opts->orthonormalizations != 1 && opts->orthonormalizations != 2)
     fail(TSSVD_EINVAL, "orthonormalizations must be 1 or 2");
   if (!rank) fail(TSSVD_EINVAL, "rank is NULL");
@@ -459,9 +618,12 @@ void tssvd_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, cons
   a.dry = false;
   TsPlan p;
   plan_tssvd(a, p, m_local, (int)n, opts);
-  c.jinfo = p.jinfo;
-  const int64_t m = global_rows(c, m_local, p.m_scratch);
-  if (m < n) fail(TSSVD_EINVAL, "m = %lld < n = %lld (the matrix must be tall, P:98-104)", (long long)m, (long long)n);
+  c.ctl = p.ctl;
+  step("tssvd:%d", opts->orthonormalizations);
+  CUR(cudaMemsetAsync(c.ctl, 0, kCtlInts * sizeof(int), c.s));
+  const int64_t m_now = global_rows(c, m_local);
+  if (m_now >= 0 && m_now < n)
+    fail(TSSVD_EINVAL, "m = %lld < n = %lld (the matrix must be tall, P:98-104)", (long long)m_now, (long long)n);
   const double* X = A;
   int64_t ldx = lda;
   double* Ud = U;
@@ -470,33 +632,43 @@ void tssvd_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, cons
   double* Vd = V;
   int64_t ldvd = ldv;
   if (hio) {  // stage host A into the workspace (it becomes the in-place U buffer)
+    const int64_t lds = even(n);
+    step("h2d:A");
     if (m_local > 0) {
-      if (lda == n) CU(cudaMemcpyAsync(p.a_stage, A, (size_t)m_local * n * 8, cudaMemcpyHostToDevice, c.s));
-      else CU(cudaMemcpy2DAsync(p.a_stage, n * 8, A, lda * 8, n * 8, m_local, cudaMemcpyHostToDevice, c.s));
+      if (lda == lds) CUR(cudaMemcpyAsync(p.a_stage, A, (size_t)m_local * n * 8, cudaMemcpyHostToDevice, c.s));
+      else CUR(cudaMemcpy2DAsync(p.a_stage, lds * 8, A, lda * 8, n * 8, m_local, cudaMemcpyHostToDevice, c.s));
     }
     X = p.a_stage;
-    ldx = n;
+    ldx = lds;
     Ud = p.a_stage;
-    ldud = n;
+    ldud = lds;
     sigd = p.sig_stage;
     Vd = p.v_stage;
     ldvd = n;
   }
   const bool packed = hio && ldu == 0;
-  const int64_t r = core(c, p.core, X, ldx, m_local, (int)n, opts->orthonormalizations, true, Ud,
-                         ldud, sigd, Vd, ldvd, packed ? p.u_pack : nullptr);
-  if (hio && r > 0) {
+  const CoreOut o = core(c, p.core, X, ldx, m_local, (int)n, opts->orthonormalizations, true, Ud, ldud, sigd,
+                         Vd, ldvd, devmode_for((int)n), packed ? p.u_pack : nullptr);
+  Finish f;
+  finish(c, f);
+  if (c.dist() && !g_dry && f.m < n)
+    fail(TSSVD_EINVAL, "m = %lld < n = %lld (the matrix must be tall, P:98-104)", (long long)f.m, (long long)n);
+  const int64_t r = core_rank(o, f);
+  if (hio && r > 0) {  // results D2H: exactly r columns (the factor buffers hold o.bound)
+    step("d2h:U");
     if (m_local > 0) {
-      if (packed)  // one contiguous copy: U with leading dimension (r + 1) & ~1
-        CU(cudaMemcpyAsync(U, p.u_pack, (size_t)m_local * ((r + 1) & ~1) * 8, cudaMemcpyDeviceToHost, c.s));
+      const int64_t pb = (o.bound + 1) & ~1, pr = (r + 1) & ~1;
+      if (packed && pb == pr)  // one contiguous copy: U with leading dimension (r + 1) & ~1
+        CUR(cudaMemcpyAsync(U, p.u_pack, (size_t)m_local * pr * 8, cudaMemcpyDeviceToHost, c.s));
+      else if (packed)
+        CUR(cudaMemcpy2DAsync(U, pr * 8, p.u_pack, pb * 8, r * 8, m_local, cudaMemcpyDeviceToHost, c.s));
       else
-        CU(cudaMemcpy2DAsync(U, ldu * 8, Ud, ldud * 8, r * 8, m_local, cudaMemcpyDeviceToHost, c.s));
+        CUR(cudaMemcpy2DAsync(U, ldu * 8, Ud, ldud * 8, r * 8, m_local, cudaMemcpyDeviceToHost, c.s));
     }
-    CU(cudaMemcpyAsync(sigma, sigd, r * 8, cudaMemcpyDeviceToHost, c.s));
-    CU(cudaMemcpy2DAsync(V, ldv * 8, Vd, ldvd * 8, r * 8, n, cudaMemcpyDeviceToHost, c.s));
+    CUR(cudaMemcpyAsync(sigma, sigd, r * 8, cudaMemcpyDeviceToHost, c.s));
+    CUR(cudaMemcpy2DAsync(V, ldv * 8, Vd, ldvd * 8, r * 8, n, cudaMemcpyDeviceToHost, c.s));
+    CUR(cudaStreamSynchronize(c.s));
   }
-  CU(cudaStreamSynchronize(c.s));
-  check_deferred(c);
   g_timer.resolve();
   *rank = r;
 }
@@ -504,8 +676,7 @@ void tssvd_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, cons
 // ------------------------------------------------------------- low rank --
 struct LrPlan {
   Core tall, small;
-  int* jinfo;
-  int64_t* m_scratch;
+  int* ctl;
   double *Qt, *Y, *Z, *tn, *Ut, *sig_tmp, *v_scr, *sig_scr, *Mfin;
   double *a_stage, *o_stage, *u_stage, *s_stage, *vo_stage;
   int lp, ldzmax;
@@ -514,8 +685,7 @@ struct LrPlan {
 size_t plan_lowrank(Arena& a, LrPlan& p, int64_t m_local, int n, int l, const tssvd_opts* o) {
   p.lp = (l + 1) & ~1;
   p.ldzmax = pad8(l);
-  p.jinfo = a.get<int>(8 * Ctx::kMaxDeferred);
-  p.m_scratch = a.get<int64_t>(2);
+  p.ctl = a.get<int>(kCtlInts);
   p.tall.alloc(a, m_local, l);
   p.small.alloc(a, n, l);
   p.Qt = a.get<double>(gemm_nn_m_doubles(n, l));
@@ -530,28 +700,33 @@ size_t plan_lowrank(Arena& a, LrPlan& p, int64_t m_local, int n, int l, const ts
   p.v_scr = a.get<double>((size_t)std::max(n, l) * l);
   p.Mfin = a.get<double>(gemm_nn_m_doubles(l, l));
   if (o && o->host_io) {
-    p.a_stage = a.get<double>((size_t)std::max<int64_t>(m_local, 1) * n);
-    p.o_stage = a.get<double>((size_t)n * l);
-    p.u_stage = a.get<double>((size_t)std::max<int64_t>(m_local, 1) * l);
+    p.a_stage = a.get<double>((size_t)std::max<int64_t>(m_local, 1) * even(n));
+    p.o_stage = a.get<double>((size_t)n * even(l));
+    p.u_stage = a.get<double>((size_t)std::max<int64_t>(m_local, 1) * even(l));  // k <= l columns
     p.s_stage = a.get<double>(l);
     p.vo_stage = a.get<double>((size_t)n * l);
   }
   return a.off;
 }
 
-// Z (n x ldz) = sum over ranks of A_p^T Q_p  (Alg. 5 step 5 / Alg. 6 step 1)
+// Z (n x ldo) = sum over ranks of A_p^T Q_p  (Alg. 5 step 5 / Alg. 6 step 1); the
+// split-K partials are summed in a fixed order on the device (36 MB per c3 pass
+// through L2/HBM, ~15 us), then allreduced WITHOUT the partials' pad columns
+// (ldo = r rounded up to even).
 int tn_pass(Ctx& c, LrPlan& p, const double* A, int64_t lda, int64_t m_local, int n, int r) {
+  step("beta:%d", r);
   const TnPlan tp = plan_gemm_tn(std::max<int64_t>(m_local, 1), n, r);
+  const int ldo = (r + 1) & ~1;
   if (m_local > 0) {
     Pass t(c.s, TSSVD_PASS_BETA, 2.0 * m_local * n * r, 8.0 * m_local * (n + r));
     KL(launch_gemm_tn(tp, A, lda, m_local, n, p.Y, p.lp, r, p.tn, c.s));
-    KL(launch_reduce_parts(p.tn, tp.splits, (int64_t)tp.colblocks * tp.cb * tp.ldz, (int64_t)n * tp.ldz, p.Z, c.s));
+    KL(launch_reduce_parts_2d(p.tn, tp.splits, (int64_t)tp.colblocks * tp.cb * tp.ldz, n, tp.ldz, r, p.Z, ldo, true, c.s));
   } else {
-    KS(fill(p.Z, (int64_t)n * tp.ldz, 0.0, c.s));
+    KS(fill(p.Z, (int64_t)n * ldo, 0.0, c.s));
   }
   ++g_stats.a_passes;
-  allreduce(c, p.Z, (int64_t)n * tp.ldz);
-  return tp.ldz;
+  allreduce(c, p.Z, (int64_t)n * ldo, "beta");
+  return ldo;
 }
 
 void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, const double* A,
@@ -561,8 +736,9 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
   g_stats = tssvd_stats{};
   check_opts(opts);
   if (m_local < 0) fail(TSSVD_EINVAL, "m_local < 0");
-  if (n < 2 || (n & 1)) fail(TSSVD_EINVAL, "n = %lld must be even and >= 2", (long long)n);
-  if (lda < n || (lda & 1)) fail(TSSVD_EINVAL, "lda must be even and >= n");
+  if (n < 2) fail(TSSVD_EINVAL, "n = %lld must be >= 2", (long long)n);
+  if (lda < n || (opts->host_io != 1 && (lda & 1)))
+    fail(TSSVD_EINVAL, "lda must be even and >= n (16-byte TMA row strides)");
   if (l < 1 || l > 128 || l >= n) fail(TSSVD_EINVAL, "need 0 < l < min(m, n) and l <= 128 (l = %lld)", (long long)l);
   if (iters < 0) fail(TSSVD_EINVAL, "iters < 0");
   if (k < 1 || k > l) fail(TSSVD_EINVAL, "need 0 < k <= l");
@@ -570,6 +746,8 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
   if (!rank) fail(TSSVD_EINVAL, "rank is NULL");
   const bool hio = opts->host_io == 1;
   if (!hio && m_local > 0 && !aligned16(A)) fail(TSSVD_EINVAL, "A must be 16-byte aligned");
+  if (!hio && m_local > 0 && (!aligned16(U) || (ldu & 1)))
+    fail(TSSVD_EINVAL, "U must be 16-byte aligned with an even ldu");
   if (!ws || !aligned16(ws)) fail(TSSVD_EINVAL, "workspace NULL or misaligned");
   set_device(comm);
   Ctx c;
@@ -583,83 +761,87 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
   a.dry = false;
   LrPlan p;
   plan_lowrank(a, p, m_local, (int)n, (int)l, opts);
-  c.jinfo = p.jinfo;
-  const int64_t m = global_rows(c, m_local, p.m_scratch);
-  if (l >= std::min<int64_t>(m, n)) fail(TSSVD_EINVAL, "need l < min(m, n) (P:705-707)");
+  c.ctl = p.ctl;
+  step("lowrank:%d:%lld:%lld", iters, (long long)l, (long long)k);
+  CUR(cudaMemsetAsync(c.ctl, 0, kCtlInts * sizeof(int), c.s));
+  const int64_t m_now = global_rows(c, m_local);
+  if (m_now >= 0 && l >= std::min<int64_t>(m_now, n)) fail(TSSVD_EINVAL, "need l < min(m, n) (P:705-707)");
   const int N = (int)n, Lc = (int)l;
   const double* Ad = A;
   int64_t ldad = lda;
   const double* Od = Omega;
   int64_t ldod = ldo;
   if (hio) {
+    step("h2d:A");
     if (m_local > 0)
-      CU(cudaMemcpy2DAsync(p.a_stage, n * 8, A, lda * 8, n * 8, m_local, cudaMemcpyHostToDevice, c.s));
-    CU(cudaMemcpy2DAsync(p.o_stage, l * 8, Omega, ldo * 8, l * 8, n, cudaMemcpyHostToDevice, c.s));
+      CUR(cudaMemcpy2DAsync(p.a_stage, even(n) * 8, A, lda * 8, n * 8, m_local, cudaMemcpyHostToDevice, c.s));
+    CUR(cudaMemcpy2DAsync(p.o_stage, even(l) * 8, Omega, ldo * 8, l * 8, n, cudaMemcpyHostToDevice, c.s));
     Ad = p.a_stage;
-    ldad = n;
+    ldad = even(n);
     Od = p.o_stage;
-    ldod = l;
+    ldod = even(l);
   }
+  // Every decision stays on the device (no host round trip until the end): the
+  // launches are sized by the block width l, and columns past a kept rank are zeros.
   // Alg. 5 step 1: Q~_0 = Omega.
-  int lj = Lc;
-  KS(rows_to_m(Od, ldod, N, lj, p.Qt, smem_ld(lj), mrows_for(N), c.s));
+  KS(rows_to_m(Od, ldod, N, Lc, p.Qt, smem_ld(Lc), mrows_for(N), c.s));
   for (int it = 0; it < iters; ++it) {
     // step 3: Y_j = A Q~_{j-1}
+    step("alpha:%d", Lc);
     {
-      Pass t(c.s, TSSVD_PASS_ALPHA, 2.0 * m_local * N * lj, 8.0 * m_local * (N + lj));
-      KL(launch_gemm_nn(Ad, ldad, m_local, N, p.Qt, lj, p.Y, p.lp, nullptr, c.s));
+      Pass t(c.s, TSSVD_PASS_ALPHA, 2.0 * m_local * N * Lc, 8.0 * m_local * (N + Lc));
+      KL(launch_gemm_nn(Ad, ldad, m_local, N, p.Qt, Lc, p.Y, p.lp, nullptr, c.s));
     }
     ++g_stats.a_passes;
     // step 4: Y_j = Q_j R_j by Alg. 3 (Q_j = U, in place in Y)
-    const int64_t r = core(c, p.tall, p.Y, p.lp, m_local, lj, 1, true, p.Y, p.lp, p.sig_scr, p.v_scr, lj);
-    if (r == 0) { *rank = 0; CU(cudaStreamSynchronize(c.s)); check_deferred(c); return; }
+    core(c, p.tall, p.Y, p.lp, m_local, Lc, 1, true, p.Y, p.lp, p.sig_scr, p.v_scr, Lc, true);
     // step 5: Y~_j = A^* Q_j
-    const int ldz = tn_pass(c, p, Ad, ldad, m_local, N, (int)r);
-    // step 6: Y~_j = Q~_j R~_j by Alg. 3 on the replicated n x r matrix
-    const int64_t r2 = core(c, p.small, p.Z, ldz, N, (int)r, 1, false, p.Z, ldz, p.sig_scr, p.v_scr, r);
-    if (r2 == 0) { *rank = 0; CU(cudaStreamSynchronize(c.s)); check_deferred(c); return; }
-    lj = (int)r2;
-    KS(rows_to_m(p.Z, ldz, N, lj, p.Qt, smem_ld(lj), mrows_for(N), c.s));
+    const int ldz = tn_pass(c, p, Ad, ldad, m_local, N, Lc);
+    // step 6: Y~_j = Q~_j R~_j by Alg. 3 on the replicated n x l matrix
+    core(c, p.small, p.Z, ldz, N, Lc, 1, false, p.Z, ldz, p.sig_scr, p.v_scr, Lc, true);
+    step("qt");
+    KS(rows_to_m(p.Z, ldz, N, Lc, p.Qt, smem_ld(Lc), mrows_for(N), c.s));
   }
   // step 8: Y = A Q~_i; step 9: Y = Q R by Alg. 4
+  step("alpha:%d", Lc);
   {
-    Pass t(c.s, TSSVD_PASS_ALPHA, 2.0 * m_local * N * lj, 8.0 * m_local * (N + lj));
-    KL(launch_gemm_nn(Ad, ldad, m_local, N, p.Qt, lj, p.Y, p.lp, nullptr, c.s));
+    Pass t(c.s, TSSVD_PASS_ALPHA, 2.0 * m_local * N * Lc, 8.0 * m_local * (N + Lc));
+    KL(launch_gemm_nn(Ad, ldad, m_local, N, p.Qt, Lc, p.Y, p.lp, nullptr, c.s));
   }
   ++g_stats.a_passes;
-  const int64_t r3 = core(c, p.tall, p.Y, p.lp, m_local, lj, 2, true, p.Y, p.lp, p.sig_scr, p.v_scr, lj);
-  if (r3 == 0) { *rank = 0; CU(cudaStreamSynchronize(c.s)); check_deferred(c); return; }
+  const CoreOut o3 = core(c, p.tall, p.Y, p.lp, m_local, Lc, 2, true, p.Y, p.lp, p.sig_scr, p.v_scr, Lc, true);
   // Alg. 6 step 1: B^T = A^* Q
-  const int ldz = tn_pass(c, p, Ad, ldad, m_local, N, (int)r3);
+  const int ldz = tn_pass(c, p, Ad, ldad, m_local, N, o3.bound);
   // Alg. 6 step 2: B^T = V Sigma U~^* by Alg. 4 (reading R6); V in place in Z
-  const int64_t r4 = core(c, p.small, p.Z, ldz, N, (int)r3, 2, false, p.Z, ldz, p.sig_tmp, p.Ut, Lc);
-  if (r4 == 0) { *rank = 0; CU(cudaStreamSynchronize(c.s)); check_deferred(c); return; }
-  KS(canon_lowrank(p.Z, ldz, N, p.Ut, Lc, (int)r3, (int)r4, c.s));
-  const int kk = (int)std::min<int64_t>(k, r4);
+  const CoreOut o4 = core(c, p.small, p.Z, ldz, N, o3.bound, 2, false, p.Z, ldz, p.sig_tmp, p.Ut, Lc, true);
+  step("canon");
+  KS(canon_lowrank(p.Z, ldz, N, p.Ut, Lc, o3.bound, c.slot(o4.slot) + kSlotR, o4.bound, c.s));
+  const int kk = (int)std::min<int64_t>(k, o4.bound);
   // Alg. 6 step 3: U = Q U~ (leading kk columns, reading R7)
-  KS(rows_to_m(p.Ut, Lc, (int)r3, kk, p.Mfin, smem_ld(kk), mrows_for((int)r3), c.s));
+  step("uout:%d", kk);
+  KS(rows_to_m(p.Ut, Lc, o3.bound, kk, p.Mfin, smem_ld(kk), mrows_for(o3.bound), c.s));
   double* Uo = hio ? p.u_stage : U;
-  int64_t lduo = hio ? kk : ldu;
-  if (!hio && m_local > 0 && (!aligned16(U) || (ldu & 1))) {
-    // unaligned caller U: produce into Y's spare space is not possible; use u via copy
-    fail(TSSVD_EINVAL, "U must be 16-byte aligned with an even ldu");
-  }
-  KL(launch_gemm_nn(p.Y, p.lp, m_local, (int)r3, p.Mfin, kk, Uo, lduo, nullptr, c.s));
+  const int64_t lduo = hio ? even(kk) : ldu;  // even: the GEMM stores double2 pairs
+  KL(launch_gemm_nn(p.Y, p.lp, m_local, o3.bound, p.Mfin, kk, Uo, lduo, nullptr, c.s));
   double* So = hio ? p.s_stage : sigma;
   double* Vo = hio ? p.vo_stage : V;
-  int64_t ldvo = hio ? kk : ldv;
+  const int64_t ldvo = hio ? kk : ldv;
   KS(copy2d(p.sig_tmp, kk, So, kk, 1, kk, c.s));
   KS(copy2d(p.Z, ldz, Vo, ldvo, N, kk, c.s));
-  if (hio) {
+  Finish f;
+  finish(c, f);
+  if (c.dist() && !g_dry && l >= std::min<int64_t>(f.m, n)) fail(TSSVD_EINVAL, "need l < min(m, n) (P:705-707)");
+  const int r = (int)std::min<int64_t>(kk, core_rank(o4, f));
+  if (hio && r > 0) {
+    step("d2h:U");
     if (m_local > 0)
-      CU(cudaMemcpy2DAsync(U, ldu * 8, Uo, lduo * 8, kk * 8, m_local, cudaMemcpyDeviceToHost, c.s));
-    CU(cudaMemcpyAsync(sigma, So, kk * 8, cudaMemcpyDeviceToHost, c.s));
-    CU(cudaMemcpy2DAsync(V, ldv * 8, Vo, ldvo * 8, kk * 8, N, cudaMemcpyDeviceToHost, c.s));
+      CUR(cudaMemcpy2DAsync(U, ldu * 8, Uo, lduo * 8, r * 8, m_local, cudaMemcpyDeviceToHost, c.s));
+    CUR(cudaMemcpyAsync(sigma, So, r * 8, cudaMemcpyDeviceToHost, c.s));
+    CUR(cudaMemcpy2DAsync(V, ldv * 8, Vo, ldvo * 8, r * 8, N, cudaMemcpyDeviceToHost, c.s));
+    CUR(cudaStreamSynchronize(c.s));
   }
-  CU(cudaStreamSynchronize(c.s));
-  check_deferred(c);
   g_timer.resolve();
-  *rank = kk;
+  *rank = r;
 }
 
 }  // namespace
@@ -758,7 +940,7 @@ int tssvd_allreduce_sum(tssvd_comm* comm, void* stream, double* buf, int64_t cou
     Ctx c;
     c.comm = comm;
     c.s = static_cast<cudaStream_t>(stream);
-    allreduce(c, buf, count);
+    allreduce(c, buf, count, "user");
     CU(cudaStreamSynchronize(c.s));
   });
 }
@@ -767,7 +949,7 @@ int tssvd_workspace_size(const tssvd_comm*, int64_t m_local, int64_t n, const ts
                          size_t* bytes) {
   return guarded([&] {
     check_opts(opts);
-    validate_tall(m_local, n, n);
+    validate_tall(m_local, n, n, true);
     if (!bytes) fail(TSSVD_EINVAL, "bytes is NULL");
     Arena a;
     TsPlan p;
@@ -806,6 +988,44 @@ int lowrank_svd(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, cons
   });
 }
 
+int tssvd_trace(int problem, int nranks, int64_t m_local, int64_t n, int64_t l, int iters, int64_t k,
+                const tssvd_opts* opts, char* buf, size_t buf_len) {
+  struct DryScope {  // restores normal operation however the run ends
+    DryScope() {
+      g_dry = true;
+      g_trace.clear();
+    }
+    ~DryScope() { g_dry = false; }
+  };
+  return guarded([&] {
+    if (problem != 1 && problem != 2) fail(TSSVD_EINVAL, "problem must be 1 (tssvd) or 2 (lowrank_svd)");
+    if (nranks < 1 || !buf || buf_len == 0) fail(TSSVD_EINVAL, "bad trace arguments");
+    check_opts(opts);
+    tssvd_opts o = *opts;
+    o.host_io = 0;
+    tssvd_comm fc;  // no NCCL communicator: a dry run never calls NCCL
+    fc.nranks = nranks;
+    fc.rank = 0;
+    // placeholder (never dereferenced) device addresses, 16-byte aligned
+    double* fake = reinterpret_cast<double*>(uintptr_t(1) << 20);
+    void* fws = reinterpret_cast<void*>(uintptr_t(1) << 40);
+    const size_t fws_bytes = size_t(1) << 46;
+    int64_t rank = 0;
+    {
+      DryScope dry;
+      const int64_t ld = even(n), lk = even(std::max<int64_t>(k, 1));
+      if (problem == 1)
+        tssvd_impl(nranks > 1 ? &fc : nullptr, nullptr, m_local, n, fake, ld, &o, fake, ld, fake, fake, n, &rank,
+                   fws, fws_bytes);
+      else
+        lowrank_impl(nranks > 1 ? &fc : nullptr, nullptr, m_local, n, fake, ld, fake, l, l, iters, k, &o, fake,
+                     lk, fake, fake, k, &rank, fws, fws_bytes);
+    }
+    if (g_trace.size() + 1 > buf_len) fail(TSSVD_ENOMEM, "trace needs %zu bytes", g_trace.size() + 1);
+    std::memcpy(buf, g_trace.c_str(), g_trace.size() + 1);
+  });
+}
+
 int tssvd_set_pass_timing(int enable) {
   g_timing = enable != 0;
   return TSSVD_OK;
@@ -831,7 +1051,7 @@ int tssvd_gram(void* stream, int64_t m, int64_t n, const double* X, int64_t ldx,
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     double* part = static_cast<double*>(ws);
     CU(launch_syrk(X, ldx, m, (int)n, part, s));
-    CU(launch_reduce_sym(part, syrk_partials_grid(m, (int)n), (int)n, G, (int)ldg, s));
+    CU(launch_reduce_sym(part, syrk_partials_grid(m, (int)n), (int)n, G, (int)ldg, nullptr, s));
     CU(cudaStreamSynchronize(s));
   });
 }
@@ -875,10 +1095,9 @@ int tssvd_matmul_tn(void* stream, int64_t m, int64_t n, int64_t l, const double*
     const TnPlan tp = plan_gemm_tn(m, (int)n, (int)l);
     double* part = static_cast<double*>(ws);
     CU(launch_gemm_tn(tp, X, ldx, m, (int)n, Y, ldy, (int)l, part, s));
-    // reduce into Z columns [0, l): reduce to a padded temp is avoided by reducing per element
-    CU(launch_reduce_parts(part, tp.splits, (int64_t)tp.colblocks * tp.cb * tp.ldz, (int64_t)n * tp.ldz, part, s));  // in place into split 0
-    copy2d(part, tp.ldz, Z, ldz, n, (int)l, s);
-    CU(cudaGetLastError());
+    // fixed-order reduction of the split-K partials straight into Z's columns [0, l)
+    CU(launch_reduce_parts_2d(part, tp.splits, (int64_t)tp.colblocks * tp.cb * tp.ldz, n, tp.ldz, (int)l,
+                              Z, (int)ldz, false, s));
     CU(cudaStreamSynchronize(s));
   });
 }
@@ -888,7 +1107,7 @@ size_t tssvd_sym_eig_workspace(int64_t n) { return ((size_t)n * n + 64) * 8; }
 int tssvd_sym_eig(void* stream, int64_t n, const double* B, int64_t ldb, double* lambda, double* Vt,
                   int64_t ldv, int max_sweeps, int* sweeps, void* ws, size_t wsb) {
   return guarded([&] {
-    if (n < 1 || n > 512 || ldb < n || ldv < n) fail(TSSVD_EINVAL, "bad sym_eig arguments");
+    if (n < 1 || n > 256 || ldb < n || ldv < n) fail(TSSVD_EINVAL, "bad sym_eig arguments (1 <= n <= 256, ldb, ldv >= n)");
     if (wsb < tssvd_sym_eig_workspace(n)) fail(TSSVD_ENOMEM, "sym_eig workspace too small");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     double* vecs = static_cast<double*>(ws);

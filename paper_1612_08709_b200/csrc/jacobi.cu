@@ -252,12 +252,18 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
   __syncthreads();
 
   int K = nslots;
+  bool nonfinite = false;
   if (a.mode == 0) {
     // ---- scale of the truncation: max diagonal of B ----
     const int n = a.n;
+    // (a NaN counts as +Inf: a non-finite Gram diagonal -- an Inf/NaN in the streamed matrix,
+    // or an overflowing column -- stops the solve with K = 0 and the non-finite flag set)
     double dmax = 0.0;
     for (int i = tid; i < n; i += JT)
-      if (i >= row0 && i < row0 + nloc) dmax = fmax(dmax, X[i * P + (i - row0)]);
+      if (i >= row0 && i < row0 + nloc) {
+        const double d = X[i * P + (i - row0)];
+        dmax = fmax(dmax, isnan(d) ? INFINITY : d);
+      }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
     if (lane == 0) s_red[warp] = dmax;
@@ -271,10 +277,12 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
     double gmax = 0.0;
     for (int q = 0; q < C; ++q) gmax = fmax(gmax, s_cand[q][0]);
     const double tabs = a.trunc * gmax;
+    nonfinite = !(gmax < INFINITY);
     cl.sync();
 
-    bool done = false;
-    {
+    bool done = nonfinite;  // non-finite diagonal: K = 0, nothing pivoted
+    K = 0;
+    if (!done) {
       if (n <= 128) {
         // ---- diagonally pivoted Cholesky with the Schur complement in registers ----
         // (every CTA of a cluster runs it redundantly -- bit-identical -- and keeps its rows)
@@ -762,6 +770,7 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
     a.info[3] = (int)((t_chol - t_start) >> 4);  // phase timings, units of 16 cycles
     a.info[4] = (int)((t_sweeps - t_chol) >> 4);
     a.info[5] = rounds;
+    a.info[6] = nonfinite ? 1 : 0;
   }
   if constexpr (C > 1) cl.sync();  // keep DSMEM alive until every CTA is done with it
 }

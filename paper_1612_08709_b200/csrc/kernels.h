@@ -19,9 +19,10 @@ int syrk_partials_grid(int64_t m, int w);
 size_t syrk_partials_doubles(int64_t m, int w);
 cudaError_t launch_syrk(const double* X, int64_t ldx, int64_t m, int w, double* part,
                         cudaStream_t s);
-// B = sum_p part[p]  (lower), written symmetric into B (ldb).
+// B = sum_p part[p]  (lower), written symmetric into B (ldb); optionally also the
+// packed lower triangle (w(w+1)/2, row-major) for a half-size allreduce.
 cudaError_t launch_reduce_sym(const double* part, int nparts, int w, double* B, int ldb,
-                              cudaStream_t s);
+                              double* packed, cudaStream_t s);
 
 // Y[:, :c] = X[:, :k] * M  (M row-major, ld = smem_ld(c), rows padded to mult. of 32
 // with zeros; c <= 256).  Optional column sums of squares partials
@@ -46,12 +47,17 @@ cudaError_t launch_gemm_tn(const TnPlan& p, const double* X, int64_t ldx, int64_
 // out[e] = sum_p part[p*stride + e] for e < len (fixed two-level order)
 cudaError_t launch_reduce_parts(const double* part, int nparts, int64_t stride, int64_t len,
                                 double* out, cudaStream_t s);
+// out[row*ldo + col] = sum_p part[p*stride + row*ldi + col], col < cols (zeros up to ldo
+// when zero_pad)
+cudaError_t launch_reduce_parts_2d(const double* part, int nparts, int64_t stride, int64_t rows,
+                                   int ldi, int cols, double* out, int ldo, bool zero_pad, cudaStream_t s);
 
 // ---- one-sided Jacobi (jacobi.cu) ----
 // EIG: B (n x n, ldb, symmetric PSD) -> k <= n eigenpairs: vals[j] descending,
 // eigenvector j (unit) contiguous at vecs + j*ldv.  Pivoted-Cholesky
 // preconditioned; pivots <= trunc * max(diag B) are dropped (k = info[2]).
-// info = {sweeps, converged, k}.  vecs may alias B.
+// info = {sweeps, converged, k, -, -, rounds, nonfinite}: a non-finite diagonal
+// entry (Inf/NaN in the streamed matrix) gives k = 0 and info[6] = 1.  vecs may alias B.
 cudaError_t launch_jacobi_eig(const double* B, int ldb, int n, double tol, double trunc,
                               int max_sweeps, double* vecs, int ldv, double* vals, int* info,
                               cudaStream_t s);

@@ -38,13 +38,16 @@ __global__ void k_rows_to_m(const double* src, int64_t lds, int k, int c, double
 
 // Discard rule.  One CTA.
 //   sig_j = sqrt(nsq_j); keep j iff sig_j >= max(sig) * sqrt(wp) (and max > 0).
-//   idx = kept indices in ascending order; out[0] = r, out[1] = nc = max kept + 1,
-//   out[2] |= 1 if the Gram diagonal (gdiag, stride gld+1) is non-finite.
+//   idx = kept indices in ascending order.  Decision slot `out` (8 ints):
+//     [0] r  [1] nc = max kept + 1  [2] non-finite flag  [3] r [4] -r [5] nc [6] -nc
+//   ([3..6] are max-allreduced across ranks by the rank-consistency guard: every
+//   rank must see max == own value).  nf (nullable): the eigensolver's non-finite
+//   flag for the Gram diagonal (an Inf/NaN in A or Omega, caught by the first pass).
 __global__ void k_discard(const double* nsq, int w, double sqrt_wp, double* sig, int* idx,
-                          int* out, const double* gdiag, int gld) {
+                          int* out, const int* nf) {
   __shared__ double smax[32];
   __shared__ int bad;
-  if (threadIdx.x == 0) bad = 0;
+  if (threadIdx.x == 0) bad = nf ? (*nf != 0) : 0;
   __syncthreads();
   double mx = 0.0;
   for (int j = threadIdx.x; j < w; j += blockDim.x) {
@@ -52,7 +55,6 @@ __global__ void k_discard(const double* nsq, int w, double sqrt_wp, double* sig,
     const double s = sqrt(fmax(v, 0.0));
     sig[j] = s;
     if (!isfinite(v)) bad = 1;
-    if (gdiag && !isfinite(gdiag[(size_t)j * (gld + 1)])) bad = 1;
     mx = fmax(mx, s);
   }
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -73,6 +75,11 @@ __global__ void k_discard(const double* nsq, int w, double sqrt_wp, double* sig,
     out[0] = r;
     out[1] = nc;
     out[2] = bad;
+    out[3] = r;
+    out[4] = -r;
+    out[5] = nc;
+    out[6] = -nc;
+    out[7] = 0;
   }
 }
 
@@ -88,13 +95,21 @@ __device__ double col_sign(const double* x, int stride, int len) {
 }
 
 // Alg. 3 outputs with reading R4 (sort by Sigma descending) and R5 (signs).
-// Vt: eigenvectors, column-major (column j at Vt + j*w).  One thread per kept column.
+// Vt: eigenvectors, column-major (column j at Vt + j*w).  One thread per output
+// position a < rb (rb = host bound >= r; r = *rr is the kept rank on the device).
 //   rank_a = position of kept column a by descending sig (ties by index)
 //   M[idx_a][rank_a] = s_a / sig[idx_a];  V[:, rank_a] = s_a * Vt[:, idx_a];  sigma[rank_a] = sig
-__global__ void k_alg3_out(const double* sig, const int* idx, int r, const double* Vt, int w,
-                           double* M, int ldm, double* sigma, double* V, int64_t ldv) {
+// Positions [r, rb) get sigma = 0 and V = 0 (M's columns there stay zero).
+__global__ void k_alg3_out(const double* sig, const int* idx, const int* rr, int rb, const double* Vt,
+                           int w, double* M, int ldm, double* sigma, double* V, int64_t ldv) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a >= r) return;
+  if (a >= rb) return;
+  const int r = *rr;
+  if (a >= r) {
+    sigma[a] = 0.0;
+    for (int i = 0; i < w; ++i) V[(size_t)i * ldv + a] = 0.0;
+    return;
+  }
   const int ja = idx[a];
   const double sa = sig[ja];
   int rk = 0;
@@ -109,58 +124,72 @@ __global__ void k_alg3_out(const double* sig, const int* idx, int r, const doubl
   for (int i = 0; i < w; ++i) V[(size_t)i * ldv + rk] = sg * v[i];
 }
 
-// Z[a][b] = G[idx_a][idx_b] / (sig_a sig_b) -- Gram of Y = Y~_keep Sigma~^-1.
-__global__ void k_build_z(const double* G, int ldg, const int* idx, const double* sig, int r,
-                          double* Z) {
+// Z[a][b] = G[idx_a][idx_b] / (sig_a sig_b) -- Gram of Y = Y~_keep Sigma~^-1;
+// rb x rb (ld rb), zero outside the leading r x r block (r = *rr).
+__global__ void k_build_z(const double* G, int ldg, const int* idx, const double* sig, const int* rr,
+                          int rb, double* Z) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= r * r) return;
-  const int a = e / r, b = e % r;
+  if (e >= rb * rb) return;
+  const int r = *rr;
+  const int a = e / rb, b = e % rb;
+  if (a >= r || b >= r) {
+    Z[e] = 0.0;
+    return;
+  }
   const int ia = idx[a], ib = idx[b];
   Z[e] = G[(size_t)ia * ldg + ib] / (sig[ia] * sig[ib]);
 }
 
-// M1 (nc x r, row-major padded): M1[idx_a][b] = W(a, b) / sig[idx_a] so that
-// Y~[:, :nc] M1 = Y~_keep Sigma~^-1 W = Y W = Q~.  W column-major (r x r).
-__global__ void k_build_m1(const double* W, const int* idx, const double* sig, int r, int kz,
-                           double* M1, int ldm) {
+// M1 (nc x kz, row-major padded, pre-zeroed): M1[idx_a][b] = W(a, b) / sig[idx_a] for a < r,
+// so that Y~[:, :nc] M1 = Y~_keep Sigma~^-1 W = Y W = Q~.  W column-major (ld ldw).
+__global__ void k_build_m1(const double* W, int ldw, const int* idx, const double* sig, const int* rr,
+                           int rb, int kz, double* M1, int ldm) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= r * kz) return;
+  if (e >= rb * kz) return;
   const int a = e / kz, b = e % kz;
+  if (a >= *rr) return;
   const int ia = idx[a];
-  M1[(size_t)ia * ldm + b] = W[(size_t)b * r + a] / sig[ia];
+  M1[(size_t)ia * ldm + b] = W[(size_t)b * ldw + a] / sig[ia];
 }
 
 // Columns of K = T_keep W_keep^T Sigma~ (r2 x r) for the SVD of R = K V~_keep^T
-// (reading R13): column b (length r2) at Kc + b*r2,
-//   K[a][b] = T[idx2_a] * W(b, idx2_a) * sig[idx_b].   W column-major (r x kz).
-__global__ void k_build_k(const double* T, const int* idx2, int r2, const double* W, int r,
-                          const double* sig, const int* idx, double* Kc) {
+// (reading R13): column b (length rb2, zero rows from r2 on) at Kc + b*rb2,
+// rb columns (zero from r on):  K[a][b] = T[idx2_a] * W(b, idx2_a) * sig[idx_b].
+__global__ void k_build_k(const double* T, const int* idx2, const int* rr2, int rb2, const double* W,
+                          int ldw, const int* rr, int rb, const double* sig, const int* idx, double* Kc) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= r2 * r) return;
-  const int b = e / r2, a = e % r2;
+  if (e >= rb2 * rb) return;
+  const int b = e / rb2, a = e % rb2;
+  if (a >= *rr2 || b >= *rr) {
+    Kc[e] = 0.0;
+    return;
+  }
   const int c2 = idx2[a];
-  Kc[e] = T[c2] * W[(size_t)c2 * r + b] * sig[idx[b]];
+  Kc[e] = T[c2] * W[(size_t)c2 * ldw + b] * sig[idx[b]];
 }
 
-// After the Jacobi SVD of K (column a of `cols`: [P(:, a) (r2) ; J(:, a) (r)]):
+// After the Jacobi SVD of K (column a of `cols`: [P(:, a) (rb2) ; J(:, a) (rb)]):
 //   V(:, a) = V~_keep J(:, a)  (R = P Sigma (V~_keep J)^T), sign fixed (R5),
-//   sigma[a], V (row-major, ldv), Ps = P * signs (column-major r2 x r2).
+//   sigma[a], V (row-major, ldv), Ps = P * signs (column-major rb2 x rb2, zero from r2 on).
+// Output columns a in [r2, rb2) (r2 = *rr2, kept rank of the second discard) are zeros.
 // One CTA per 8 output columns; thread i computes row i of V(:, a0:a0+8).
 static constexpr int SVO_COLS = 8;
-__global__ void __launch_bounds__(256) k_svd_out(const double* cols, int ldc, int r2, int r,
-                                                 const double* vals, const double* Vt, int w,
-                                                 const int* idx, double* sigma, double* V, int64_t ldv,
-                                                 double* Ps) {
+__global__ void __launch_bounds__(256) k_svd_out(const double* cols, int ldc, const int* rr2, int rb2,
+                                                 const int* rr, const double* vals, const double* Vt,
+                                                 int w, const int* idx, double* sigma, double* V,
+                                                 int64_t ldv, double* Ps) {
   __shared__ double sJ[256][SVO_COLS];
   __shared__ int sidx[256];
   __shared__ double sbest[8][SVO_COLS];
   __shared__ int sbi[8][SVO_COLS];
   __shared__ double ssign[SVO_COLS];
+  const int r2 = *rr2, r = *rr;
   const int a0 = blockIdx.x * SVO_COLS, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int na = min(SVO_COLS, r2 - a0);
+  const int nall = min(SVO_COLS, rb2 - a0);           // output columns of this CTA
+  const int na = max(0, min(SVO_COLS, r2 - a0));      // ... that are real
   for (int e = tid; e < r * SVO_COLS; e += blockDim.x) {
     const int bb = e / SVO_COLS, q = e % SVO_COLS;
-    sJ[bb][q] = q < na ? cols[(size_t)(a0 + q) * ldc + r2 + bb] : 0.0;
+    sJ[bb][q] = q < na ? cols[(size_t)(a0 + q) * ldc + rb2 + bb] : 0.0;
   }
   for (int bb = tid; bb < r; bb += blockDim.x) sidx[bb] = idx[bb];
   __syncthreads();
@@ -204,32 +233,35 @@ __global__ void __launch_bounds__(256) k_svd_out(const double* cols, int ldc, in
   if (i < w)
 #pragma unroll
     for (int q = 0; q < SVO_COLS; ++q)
-      if (q < na) V[(size_t)i * ldv + a0 + q] = ssign[q] * v[q];
-  for (int e = tid; e < na * r2; e += blockDim.x) {
-    const int q = e / r2, c = e % r2;
-    Ps[(size_t)(a0 + q) * r2 + c] = ssign[q] * cols[(size_t)(a0 + q) * ldc + c];
+      if (q < nall) V[(size_t)i * ldv + a0 + q] = q < na ? ssign[q] * v[q] : 0.0;
+  for (int e = tid; e < nall * rb2; e += blockDim.x) {
+    const int q = e / rb2, c = e % rb2;
+    Ps[(size_t)(a0 + q) * rb2 + c] = (q < na && c < r2) ? ssign[q] * cols[(size_t)(a0 + q) * ldc + c] : 0.0;
   }
-  if (tid < na) sigma[a0 + tid] = vals[a0 + tid];
+  if (tid < nall) sigma[a0 + tid] = tid < na ? vals[a0 + tid] : 0.0;
 }
 
-// M2 (nc x r2 row-major padded): M2[idx_b][a] = sum_c W(b, idx2_c) / (sig[idx_b] T[idx2_c]) Ps(c, a)
-// so that Y~[:, :nc] M2 = Q~_keep T^-1 P = Q P = U.
-__global__ void __launch_bounds__(256) k_build_m2(const double* W, int r, const int* idx, const double* sig,
-                                                   const double* T, const int* idx2, int r2, const double* Ps,
-                                                   double* M2, int ldm) {
+// M2 (nc x r2 row-major padded, pre-zeroed): M2[idx_b][a] = sum_c W(b, idx2_c) / (sig[idx_b] T[idx2_c]) Ps(c, a)
+// so that Y~[:, :nc] M2 = Q~_keep T^-1 P = Q P = U.  b < r = *rr, a, c < r2 = *rr2.
+__global__ void __launch_bounds__(256) k_build_m2(const double* W, int ldw, const int* rr, const int* idx,
+                                                   const double* sig, const double* T, const int* idx2,
+                                                   const int* rr2, int ldp, const double* Ps, double* M2,
+                                                   int ldm) {
   // one CTA per row b: wrow[c] = W(b, idx2_c) / T[idx2_c] staged once, then thread a
   // forms sum_c wrow[c] Ps(c, a) in a fixed order
   __shared__ double wrow[256];
   const int b = blockIdx.x;
+  if (b >= *rr) return;
+  const int r2 = *rr2;
   for (int c = threadIdx.x; c < r2; c += blockDim.x) {
     const int c2 = idx2[c];
-    wrow[c] = W[(size_t)c2 * r + b] / T[c2];
+    wrow[c] = W[(size_t)c2 * ldw + b] / T[c2];
   }
   __syncthreads();
   const int ib = idx[b];
   const double inv = 1.0 / sig[ib];
   for (int a = threadIdx.x; a < r2; a += blockDim.x) {
-    const double* pa = Ps + (size_t)a * r2;
+    const double* pa = Ps + (size_t)a * ldp;
     double s = 0.0;
 #pragma unroll 8
     for (int c = 0; c < r2; ++c) s = fma(wrow[c], pa[c], s);
@@ -237,15 +269,26 @@ __global__ void __launch_bounds__(256) k_build_m2(const double* W, int r, const 
   }
 }
 
+// Packed lower triangle (w(w+1)/2, row-major (i, j<=i)) -> symmetric B (ldb).  Used after
+// the allreduce of the packed Gram (half the bytes of the full matrix).
+__global__ void k_unpack_sym(const double* packed, int w, double* B, int ldb) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= w * w) return;
+  const int i = e / w, j = e % w;
+  const int hi = max(i, j), lo = min(i, j);
+  B[(size_t)i * ldb + j] = packed[(size_t)hi * (hi + 1) / 2 + lo];
+}
+
 // Low-rank final step: flip (V_A[:, a], Ut(:, a)) so V_A's largest entry is positive (R5),
-// V_A row-major (n x ?, ldva), Ut row-major (r3 x r4, ldu_t).  One thread per column.
+// V_A row-major (n x ?, ldva), Ut row-major (r3 x r4, ldu_t).  Columns a < r4 = *rr4.
 __global__ void __launch_bounds__(256) k_canon_lowrank(double* VA, int64_t ldva, int n, double* Ut, int ldut,
-                                                        int r3, int r4) {
+                                                        int r3, const int* rr4) {
   // one CTA per column a: block argmax of |V_A(:, a)| (ties -> lowest row), then a parallel flip
   __shared__ double sv[8];
   __shared__ int si[8];
   __shared__ double sgn;
   const int a = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (a >= *rr4) return;
   double bv = -1.0, val = 0.0;
   int bi = 1 << 30;
   for (int i = tid; i < n; i += blockDim.x) {
@@ -299,6 +342,9 @@ static inline unsigned nb(int64_t n, int b = 256) { return (unsigned)((n + b - 1
 void symmetrize(double* B, int w, int ldb, cudaStream_t s) {
   k_symmetrize<<<nb((int64_t)w * w), 256, 0, s>>>(B, w, ldb);
 }
+void unpack_sym(const double* packed, int w, double* B, int ldb, cudaStream_t s) {
+  k_unpack_sym<<<nb((int64_t)w * w), 256, 0, s>>>(packed, w, B, ldb);
+}
 void cols_to_m(const double* cols, int ldc, int k, int c, double* M, int ldm, int mrows,
                cudaStream_t s) {
   k_cols_to_m<<<nb((int64_t)mrows * ldm), 256, 0, s>>>(cols, ldc, k, c, M, ldm, mrows);
@@ -307,38 +353,40 @@ void rows_to_m(const double* src, int64_t lds, int k, int c, double* M, int ldm,
                cudaStream_t s) {
   k_rows_to_m<<<nb((int64_t)mrows * ldm), 256, 0, s>>>(src, lds, k, c, M, ldm, mrows);
 }
-void discard(const double* nsq, int w, double wp, double* sig, int* idx, int* out,
-             const double* gdiag, int gld, cudaStream_t s) {
-  k_discard<<<1, 256, 0, s>>>(nsq, w, sqrt(wp), sig, idx, out, gdiag, gld);
-}
-void alg3_out(const double* sig, const int* idx, int r, const double* Vt, int w, double* M, int ldm,
-              double* sigma, double* V, int64_t ldv, cudaStream_t s) {
-  k_alg3_out<<<nb(r, 64), 64, 0, s>>>(sig, idx, r, Vt, w, M, ldm, sigma, V, ldv);
-}
-void build_z(const double* G, int ldg, const int* idx, const double* sig, int r, double* Z,
+void discard(const double* nsq, int w, double wp, double* sig, int* idx, int* out, const int* nf,
              cudaStream_t s) {
-  k_build_z<<<nb((int64_t)r * r), 256, 0, s>>>(G, ldg, idx, sig, r, Z);
+  k_discard<<<1, 256, 0, s>>>(nsq, w, sqrt(wp), sig, idx, out, nf);
 }
-void build_m1(const double* W, const int* idx, const double* sig, int r, int kz, double* M1,
+void alg3_out(const double* sig, const int* idx, const int* rr, int rb, const double* Vt, int w,
+              double* M, int ldm, double* sigma, double* V, int64_t ldv, cudaStream_t s) {
+  if (rb > 0) k_alg3_out<<<nb(rb, 64), 64, 0, s>>>(sig, idx, rr, rb, Vt, w, M, ldm, sigma, V, ldv);
+}
+void build_z(const double* G, int ldg, const int* idx, const double* sig, const int* rr, int rb,
+             double* Z, cudaStream_t s) {
+  if (rb > 0) k_build_z<<<nb((int64_t)rb * rb), 256, 0, s>>>(G, ldg, idx, sig, rr, rb, Z);
+}
+void build_m1(const double* W, int ldw, const int* idx, const double* sig, const int* rr, int rb,
+              int kz, double* M1, int ldm, cudaStream_t s) {
+  if (rb > 0 && kz > 0) k_build_m1<<<nb((int64_t)rb * kz), 256, 0, s>>>(W, ldw, idx, sig, rr, rb, kz, M1, ldm);
+}
+void build_k(const double* T, const int* idx2, const int* rr2, int rb2, const double* W, int ldw,
+             const int* rr, int rb, const double* sig, const int* idx, double* Kc, cudaStream_t s) {
+  if (rb > 0 && rb2 > 0)
+    k_build_k<<<nb((int64_t)rb2 * rb), 256, 0, s>>>(T, idx2, rr2, rb2, W, ldw, rr, rb, sig, idx, Kc);
+}
+void svd_out(const double* cols, int ldc, const int* rr2, int rb2, const int* rr, const double* vals,
+             const double* Vt, int w, const int* idx, double* sigma, double* V, int64_t ldv, double* Ps,
+             cudaStream_t s) {
+  if (rb2 > 0) k_svd_out<<<nb(rb2, SVO_COLS), 256, 0, s>>>(cols, ldc, rr2, rb2, rr, vals, Vt, w, idx, sigma, V, ldv, Ps);
+}
+void build_m2(const double* W, int ldw, const int* rr, int rb, const int* idx, const double* sig,
+              const double* T, const int* idx2, const int* rr2, int ldp, const double* Ps, double* M2,
               int ldm, cudaStream_t s) {
-  k_build_m1<<<nb((int64_t)r * kz), 256, 0, s>>>(W, idx, sig, r, kz, M1, ldm);
+  if (rb > 0 && ldp > 0) k_build_m2<<<rb, 256, 0, s>>>(W, ldw, rr, idx, sig, T, idx2, rr2, ldp, Ps, M2, ldm);
 }
-void build_k(const double* T, const int* idx2, int r2, const double* W, int r, const double* sig,
-             const int* idx, double* Kc, cudaStream_t s) {
-  k_build_k<<<nb((int64_t)r2 * r), 256, 0, s>>>(T, idx2, r2, W, r, sig, idx, Kc);
-}
-void svd_out(const double* cols, int ldc, int r2, int r, const double* vals, const double* Vt,
-             int w, const int* idx, double* sigma, double* V, int64_t ldv, double* Ps,
-             cudaStream_t s) {
-  k_svd_out<<<nb(r2, SVO_COLS), 256, 0, s>>>(cols, ldc, r2, r, vals, Vt, w, idx, sigma, V, ldv, Ps);
-}
-void build_m2(const double* W, int r, const int* idx, const double* sig, const double* T,
-              const int* idx2, int r2, const double* Ps, double* M2, int ldm, cudaStream_t s) {
-  if (r > 0 && r2 > 0) k_build_m2<<<r, 256, 0, s>>>(W, r, idx, sig, T, idx2, r2, Ps, M2, ldm);
-}
-void canon_lowrank(double* VA, int64_t ldva, int n, double* Ut, int ldut, int r3, int r4,
+void canon_lowrank(double* VA, int64_t ldva, int n, double* Ut, int ldut, int r3, const int* rr4, int rb4,
                    cudaStream_t s) {
-  if (r4 > 0) k_canon_lowrank<<<r4, 256, 0, s>>>(VA, ldva, n, Ut, ldut, r3, r4);
+  if (rb4 > 0) k_canon_lowrank<<<rb4, 256, 0, s>>>(VA, ldva, n, Ut, ldut, r3, rr4);
 }
 void copy2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int cols,
             cudaStream_t s) {

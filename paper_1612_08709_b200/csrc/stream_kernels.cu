@@ -310,7 +310,7 @@ __device__ __forceinline__ double warp_sum_parts(const double* p, int np, size_t
 }
 
 __global__ void reduce_sym_kernel(const double* __restrict__ part, int np, int w, int wp,
-                                  double* __restrict__ B, int ldb) {
+                                  double* __restrict__ B, int ldb, double* __restrict__ packed) {
   const int e = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (e >= w * (w + 1) / 2) return;
   int i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);  // lower-triangle index e -> (i, j), j <= i
@@ -321,13 +321,15 @@ __global__ void reduce_sym_kernel(const double* __restrict__ part, int np, int w
   if (lane == 0) {
     B[(size_t)i * ldb + j] = v;
     B[(size_t)j * ldb + i] = v;
+    if (packed) packed[e] = v;
   }
 }
 
-cudaError_t launch_reduce_sym(const double* part, int np, int w, double* B, int ldb,
+cudaError_t launch_reduce_sym(const double* part, int np, int w, double* B, int ldb, double* packed,
                               cudaStream_t s) {
   const int64_t threads = (int64_t)w * (w + 1) / 2 * 32;
-  reduce_sym_kernel<<<(int)ceil_div(threads, 256), 256, 0, s>>>(part, np, w, pad8(w), B, ldb);
+  if (threads == 0) return cudaSuccess;
+  reduce_sym_kernel<<<(int)ceil_div(threads, 256), 256, 0, s>>>(part, np, w, pad8(w), B, ldb, packed);
   return cudaGetLastError();
 }
 
@@ -365,6 +367,41 @@ cudaError_t launch_reduce_parts(const double* part, int np, int64_t stride, int6
     reduce_parts_long_kernel<<<(int)ceil_div(len, 256), 256, 0, s>>>(part, np, stride, len, out);
   else
     reduce_parts_kernel<<<(int)ceil_div(len * 32, 256), 256, 0, s>>>(part, np, stride, len, out);
+  return cudaGetLastError();
+}
+
+// 2-D variant for the n x l partials of A^T Q (ld ldi inside each partial): out[row*ldo + col]
+// for col < cols (zeros up to ldo when zero_pad); the partials' pad columns never leave the kernel (the
+// allreduce then moves n x ldo doubles, ldo = l rounded up to even, not n x pad8(l)).
+__global__ void reduce_parts_2d_kernel(const double* __restrict__ part, int np, int64_t stride,
+                                       int64_t rows, int ldi, int cols, double* __restrict__ out,
+                                       int ldo, int zero_pad) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= rows * ldo) return;
+  const int64_t row = e / ldo;
+  const int col = (int)(e % ldo);
+  if (col >= cols) {
+    if (zero_pad) out[e] = 0.0;
+    return;
+  }
+  const double* p = part + row * ldi + col;
+  int gs = 1;
+  while (gs * gs < np) ++gs;
+  double tot = 0.0;
+  for (int p0 = 0; p0 < np; p0 += gs) {
+    double sum = 0.0;
+    const int p1 = min(np, p0 + gs);
+    for (int q = p0; q < p1; ++q) sum += p[(size_t)q * stride];
+    tot += sum;
+  }
+  out[e] = tot;
+}
+
+cudaError_t launch_reduce_parts_2d(const double* part, int np, int64_t stride, int64_t rows, int ldi,
+                                   int cols, double* out, int ldo, bool zero_pad, cudaStream_t s) {
+  if (rows <= 0) return cudaSuccess;
+  reduce_parts_2d_kernel<<<(int)ceil_div(rows * ldo, 256), 256, 0, s>>>(part, np, stride, rows, ldi,
+                                                                         cols, out, ldo, zero_pad);
   return cudaGetLastError();
 }
 

@@ -49,7 +49,7 @@ def test_workspace_queries_and_validation_without_gpu():
     assert h.lowrank_workspace_size(None, 200_000, 20_000, 25, ctypes.byref(o), ctypes.byref(nb)) == 0
     assert nb.value > 200_000 * 26 * 8  # holds Y (m x l)
     # argument errors are reported, not crashed on
-    assert h.tssvd_workspace_size(None, 100, 7, ctypes.byref(o), ctypes.byref(nb)) == 1  # odd n
+    assert h.tssvd_workspace_size(None, 100, 7, ctypes.byref(o), ctypes.byref(nb)) == 0  # odd n is fine
     assert h.tssvd_workspace_size(None, 100, 300, ctypes.byref(o), ctypes.byref(nb)) == 1  # n > 256
     bad = _lib.default_opts(wp=1.5)
     assert h.tssvd_workspace_size(None, 100, 10, ctypes.byref(bad), ctypes.byref(nb)) == 1

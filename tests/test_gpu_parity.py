@@ -5,7 +5,7 @@ import pytest
 
 import oracle
 import synth
-from parity import assert_tssvd_parity, col_dist
+from parity import assert_lowrank_parity, assert_tssvd_parity
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -192,10 +192,13 @@ def test_tssvd_zero_matrix_and_errors():
     bad[5, 3] = float("nan")
     with pytest.raises(TssvdError, match="ENONFINITE"):
         tk.tssvd(bad)
+    wide = torch.ones((100, 11), dtype=torch.float64, device=DEV)
     with pytest.raises(TssvdError, match="EINVAL"):
-        tk.tssvd(torch.ones((100, 9), dtype=torch.float64, device=DEV))  # odd n
+        tk.tssvd(wide[:, :9])  # odd leading dimension (TMA needs 16-byte row strides)
     with pytest.raises(TssvdError, match="EINVAL"):
         tk.tssvd(torch.ones((8, 10), dtype=torch.float64, device=DEV))  # wide
+    with pytest.raises(TssvdError, match="EINVAL"):
+        tk.sym_eig(torch.eye(300, dtype=torch.float64, device=DEV))  # n > 256: EINVAL, not ECUDA
 
 
 def test_tssvd_host_io_matches_device():
@@ -221,19 +224,15 @@ def lowrank_gpu(a, om, iters, k, wp=1e-11):
     return u.cpu().numpy(), s.cpu().numpy(), v.cpu().numpy()
 
 
-@pytest.mark.parametrize("name,m,n", [("c3", 20_000, 4_000), ("c5", 25_000, 4_000)])
+@pytest.mark.parametrize("name,m,n", [("c3", 20_000, 4_000), ("c5", 25_000, 4_000), ("c3", 12_345, 2_001)])
 def test_lowrank_reduced_configs(name, m, n):
+    """c3 / c5 recipes at reduced size (n = 2001: odd width) against the oracle: sigma, U and V
+    columns within the Q11 bound, orthonormality, spectral error."""
     d = synth.config_inputs(name, m=m, n=n)
     gpu = lowrank_gpu(d["A"], d["Omega"], d["iters"], d["k"])
     ref = oracle.lowrank_svd(d["A"], d["Omega"], d["iters"], d["k"])
     assert gpu[1].size == ref[1].size == d["k"]
-    s1 = ref[1][0]
-    assert np.max(np.abs(gpu[1] - ref[1])) <= 1e-10 * s1
-    assert oracle.ortho_error(gpu[0]) <= 1e-13 and oracle.ortho_error(gpu[2]) <= 1e-13
-    eg = oracle.spectral_error(d["A"], *gpu, d["x0"])
-    er = oracle.spectral_error(d["A"], *ref, d["x0"])
-    assert abs(eg - er) <= 0.01 * er
-    assert np.all(col_dist(gpu[2], ref[2]) <= 1e-6)
+    print(assert_lowrank_parity(gpu, ref, d["A"], d["x0"]))
 
 
 @pytest.mark.parametrize("iters", [0, 1])
@@ -242,7 +241,7 @@ def test_lowrank_iters_edge(iters):
     gpu = lowrank_gpu(d["A"], d["Omega"], iters, 20)
     ref = oracle.lowrank_svd(d["A"], d["Omega"], iters, 20)
     assert gpu[1].size == ref[1].size
-    assert np.max(np.abs(gpu[1] - ref[1])) <= 1e-10 * ref[1][0]
+    print(assert_lowrank_parity(gpu, ref, d["A"], d["x0"]))
 
 
 def test_lowrank_paper_table8_pin():
@@ -252,8 +251,11 @@ def test_lowrank_paper_table8_pin():
     gpu = lowrank_gpu(a, om, 2, 20)
     ref = oracle.lowrank_svd(a, om, 2, 20)
     assert gpu[1].size == ref[1].size == 6
-    err = oracle.spectral_error(a, *gpu, synth.power_start(2_000, 7))
+    x0 = synth.power_start(2_000, 7)
+    err = oracle.spectral_error(a, *gpu, x0)
     assert err == pytest.approx(4.83e-07, rel=5e-3)
+    # U, V columns: sigma_1 / sigma_6 = 1e5 here, so the Q11 bound is loose for the last ones
+    print(assert_lowrank_parity(gpu, ref, a, x0))
 
 
 @pytest.mark.slow
@@ -351,12 +353,7 @@ def test_lowrank_l128():
     gpu = lowrank_gpu(a, om, 2, 100)
     ref = oracle.lowrank_svd(a, om, 2, 100)
     assert gpu[1].size == ref[1].size == 100
-    assert np.max(np.abs(gpu[1] - ref[1])) <= 1e-10 * ref[1][0]
-    assert oracle.ortho_error(gpu[0]) <= 1e-13 and oracle.ortho_error(gpu[2]) <= 1e-13
-    x0 = synth.power_start(n, 5)
-    eg = oracle.spectral_error(a, *gpu, x0)
-    er = oracle.spectral_error(a, *ref, x0)
-    assert abs(eg - er) <= 0.01 * er
+    print(assert_lowrank_parity(gpu, ref, a, synth.power_start(n, 5)))
 
 
 def test_comm_wrap_nccl_borrows_torch_communicator():
@@ -380,3 +377,180 @@ def test_comm_wrap_nccl_borrows_torch_communicator():
     comm.close()
     pg.allreduce([x]).wait()
     assert torch.equal(x.cpu(), torch.ones(4))
+
+
+# ------------------------------------------------ boundary and edge cases --
+@pytest.mark.parametrize("m,n,passes", [(10_000, 25, 2), (50_001, 99, 2), (7_777, 33, 1), (3_000, 1, 2)])
+def test_tssvd_odd_n(m, n, passes):
+    """Odd widths (even leading dimension): n = 25 / 33 run the device-side-decision path
+    (n <= 32 / n > 32), n = 99 the host-decision path, n = 1 the degenerate single column."""
+    rng = np.random.default_rng(m + n)
+    sig = 10.0 ** (-8.0 * np.arange(n) / max(n - 1, 1))
+    u, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    a = (u * sig) @ v.T
+    gpu = run_tssvd(a, 1e-11, passes)
+    ref = oracle.tssvd(a, 1e-11, passes)
+    print(assert_tssvd_parity(gpu, ref, passes=passes))
+
+
+@pytest.mark.parametrize("name,m", [("c1", None), ("c2", 100_000)])
+def test_enoconv(name, m):
+    """max_jacobi_sweeps = 1: the eigensolvers cannot converge -> TSSVD_ENOCONV (c1: a deferred
+    device-side check; c2: the host-read eigensolver of the first pass)."""
+    d = synth.config_inputs(name, m=m)
+    with pytest.raises(TssvdError, match="ENOCONV"):
+        tk.tssvd(to_dev(d["A"]), max_sweeps=1)
+    dl = synth.config_inputs("c3", m=3_000, n=500)
+    with pytest.raises(TssvdError, match="ENOCONV"):
+        tk.lowrank_svd(to_dev(dl["A"]), to_dev(dl["Omega"]), 1, 10, max_sweeps=1)
+
+
+@pytest.mark.parametrize("bad", [float("inf"), float("-inf"), float("nan")])
+def test_nonfinite_inputs(bad):
+    """Inf / NaN anywhere in A (or Omega) -> TSSVD_ENONFINITE from the first pass's Gram
+    diagonal, on the narrow (device-decision) and wide (host-decision) paths and in Alg. 8;
+    the library stays usable afterwards."""
+    for m, n in [(4000, 10), (20_000, 100)]:
+        a = np.random.default_rng(n).standard_normal((m, n))
+        a[m // 3, n // 2] = bad
+        with pytest.raises(TssvdError, match="ENONFINITE"):
+            tk.tssvd(to_dev(a))
+    d = synth.config_inputs("c3", m=3_000, n=500)
+    a = d["A"].copy()
+    a[17, 400] = bad
+    with pytest.raises(TssvdError, match="ENONFINITE"):
+        tk.lowrank_svd(to_dev(a), to_dev(d["Omega"]), 1, 10)
+    om = d["Omega"].copy()
+    om[3, 2] = bad
+    with pytest.raises(TssvdError, match="ENONFINITE"):
+        tk.lowrank_svd(to_dev(d["A"]), to_dev(om), 1, 10)
+    ok = tk.tssvd(to_dev(synth.config_inputs("c1")["A"]))
+    assert ok[1].numel() == 9
+
+
+@pytest.mark.parametrize("k", [5, 20])
+def test_lowrank_host_io_odd_k(k):
+    """CPU tensors (host_io) with odd k: U is staged with an even leading dimension (ADVICE r1:
+    odd lduo misaligned the GEMM's 16-byte stores); identical to the device API."""
+    d = synth.config_inputs("c3", m=5_001, n=999)
+    a, om = torch.from_numpy(d["A"]), torch.from_numpy(d["Omega"])
+    uh, sh, vh = tk.lowrank_svd(a.pin_memory(), om.pin_memory(), d["iters"], k)
+    ud, sd, vd = tk.lowrank_svd(a.to(DEV), om.to(DEV), d["iters"], k)
+    assert sh.numel() == k
+    assert torch.equal(sh, sd.cpu()) and torch.equal(vh, vd.cpu()) and torch.equal(uh, ud.cpu())
+
+
+def _subprocess_parity(env_extra, code):
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, **env_extra)
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=900)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-3000:]
+    return out.stdout
+
+
+DEVMODE_CODE = """
+import sys; sys.path.insert(0, 'tests'); sys.path.insert(0, '.')
+import numpy as np, torch, oracle, synth, paper_1612_08709_b200 as tk
+from parity import assert_tssvd_parity
+for name, m in [("c1", None), ("c2", 200_000), ("c4", 200_000)]:
+    d = synth.config_inputs(name, m=m)
+    u, s, v = tk.tssvd(torch.from_numpy(d["A"]).cuda())
+    gpu = (u.cpu().numpy(), s.cpu().numpy(), v.cpu().numpy())
+    print(name, tk.last_stats()["ranks"], assert_tssvd_parity(gpu, oracle.tssvd(d["A"], 1e-11, 2), passes=2))
+"""
+
+
+@pytest.mark.parametrize("mode", ["1", "0"])
+def test_tssvd_decision_modes(mode):
+    """TSSVD_DEVICE_RANK=1 runs the wide cores (c2, c4) with every rank decision on the
+    device (bound-sized launches), =0 runs the narrow c1 core with host round trips: both
+    must meet the same parity contract as the default split."""
+    print(_subprocess_parity({"TSSVD_DEVICE_RANK": mode}, DEVMODE_CODE))
+
+
+# ------------------------------------------------------- full-size configs --
+def _host_gib():
+    import psutil
+
+    return psutil.virtual_memory().available / 2**30
+
+
+@pytest.mark.slow
+def test_tssvd_c4_full_size_oracle():
+    """BASELINE configs[3] against the oracle at the largest m the host's memory allows (the
+    oracle holds ~8 copies of m x 200; full size 8e6 rows needs ~110 GB)."""
+    m = int(min(8_000_000, _host_gib() * 2**30 * 0.7 / (8 * 200 * 9)))
+    if m < 1_000_000:
+        pytest.skip(f"host memory too small for a useful c4 oracle run ({_host_gib():.0f} GiB)")
+    d = synth.config_inputs("c4", m=m)
+    gpu = run_tssvd(d["A"], 1e-11, 2)
+    ref = oracle.tssvd(d["A"], 1e-11, 2)
+    assert ref[1].size == 92
+    info = assert_tssvd_parity(gpu, ref, passes=2)
+    print("c4 m =", m, info)
+
+
+@pytest.mark.slow
+def test_lowrank_c3_full_size_oracle():
+    """BASELINE configs[2] at full size (200,000 x 20,000, 32 GB) against the oracle: the
+    same contract as the reduced cases (needs ~70 GB of host memory)."""
+    if _host_gib() < 80:
+        pytest.skip(f"host memory too small for the full c3 oracle ({_host_gib():.0f} GiB)")
+    d = synth.config_inputs("c3")
+    gpu = lowrank_gpu(d["A"], d["Omega"], d["iters"], d["k"])
+    ref = oracle.lowrank_svd(d["A"], d["Omega"], d["iters"], d["k"])
+    info = assert_lowrank_parity(gpu, ref, d["A"], d["x0"])
+    assert abs(info["spectral_error_gpu"] - d["sigma"][d["k"]]) <= 0.01 * d["sigma"][d["k"]]
+    print(info)
+
+
+@pytest.mark.slow
+def test_lowrank_c5_full_size_properties():
+    """BASELINE configs[4] (500,000 x 40,000 FP64 = 160 GB) on ONE B200 (BASELINE lists it for
+    2/4/8 GPUs; one GPU's HBM still holds it).  A is built on the device with torch's generator
+    (same recipe as synth: A = U_r diag(sigma) V_r^T + 1e-8 G / sqrt(n), Haar U_r, V_r,
+    sigma_j = exp(-(j-1)/15), r = 100) -- 160 GB do not fit the host, so there is no oracle at
+    this size.  Properties that hold at any size: sigma_1..k against the constructed spectrum
+    (Weyl: |d sigma| <= ||noise||_2), U and V orthonormal, the rank-k spectral error (20 power
+    iterations) against sigma_{k+1}."""
+    import math
+
+    free, _ = torch.cuda.mem_get_info()
+    m, n, r, k, l, iters = 500_000, 40_000, 100, 50, 60, 4
+    if free < 8 * m * n + (12 << 30):
+        pytest.skip("not enough device memory for c5 on one GPU")
+    f64 = torch.float64
+    g = torch.Generator(device=DEV).manual_seed(5)
+    ur, _ = torch.linalg.qr(torch.randn(m, r, generator=g, device=DEV, dtype=f64))
+    vr, _ = torch.linalg.qr(torch.randn(n, r, generator=g, device=DEV, dtype=f64))
+    sigma = torch.exp(-torch.arange(r, device=DEV, dtype=f64) / 15.0)
+    b = sigma[:, None] * vr.T
+    A = torch.empty((m, n), device=DEV, dtype=f64)
+    for i in range(0, m, 2048):
+        j = min(m, i + 2048)
+        torch.randn((j - i, n), generator=g, device=DEV, dtype=f64, out=A[i:j])
+        A[i:j].mul_(1e-8 / math.sqrt(n)).addmm_(ur[i:j], b)
+    del ur, vr, b
+    omega = torch.randn((n, l), generator=g, device=DEV, dtype=f64)
+    U, S, V = tk.lowrank_svd(A, omega, iters, k)
+    torch.cuda.synchronize()
+    assert S.numel() == k
+    noise = 1e-8 * (math.sqrt(m) + math.sqrt(n)) / math.sqrt(n) * 1.1
+    assert (S - sigma[:k]).abs().max().item() <= noise + 1e-10
+    eye = torch.eye(k, device=DEV, dtype=f64)
+    assert (U.T @ U - eye).abs().max().item() <= 1e-13
+    assert (V.T @ V - eye).abs().max().item() <= 1e-13
+    x = torch.randn(n, generator=g, device=DEV, dtype=f64)
+    for _ in range(20):
+        y = A @ x - U @ (S * (V.T @ x))
+        x = A.T @ y - V @ (S * (U.T @ y))
+        x /= torch.linalg.norm(x)
+    err = torch.linalg.norm(A @ x - U @ (S * (V.T @ x))).item()
+    sk1 = math.exp(-k / 15.0)
+    assert abs(err - sk1) <= 0.01 * sk1 + noise
