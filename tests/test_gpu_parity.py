@@ -20,7 +20,14 @@ DEV = torch.device("cuda", 0)
 
 
 def to_dev(a):
-    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+    """Device copy with an EVEN leading dimension (the C ABI's 16-byte row-stride rule): an odd
+    width gets one pad column, and the returned tensor is the [:, :n] view of it."""
+    a = np.ascontiguousarray(a)
+    if a.ndim == 2 and a.shape[1] & 1:
+        buf = torch.zeros((a.shape[0], a.shape[1] + 1), dtype=torch.float64, device=DEV)
+        buf[:, :a.shape[1]] = torch.from_numpy(a).to(DEV)
+        return buf[:, :a.shape[1]]
+    return torch.from_numpy(a).to(DEV)
 
 
 def run_tssvd(a, wp, passes, **kw):
@@ -435,8 +442,8 @@ def test_lowrank_host_io_odd_k(k):
     odd lduo misaligned the GEMM's 16-byte stores); identical to the device API."""
     d = synth.config_inputs("c3", m=5_001, n=999)
     a, om = torch.from_numpy(d["A"]), torch.from_numpy(d["Omega"])
-    uh, sh, vh = tk.lowrank_svd(a.pin_memory(), om.pin_memory(), d["iters"], k)
-    ud, sd, vd = tk.lowrank_svd(a.to(DEV), om.to(DEV), d["iters"], k)
+    uh, sh, vh = tk.lowrank_svd(a.pin_memory(), om.pin_memory(), d["iters"], k)  # odd lda is fine here
+    ud, sd, vd = tk.lowrank_svd(to_dev(d["A"]), om.to(DEV), d["iters"], k)
     assert sh.numel() == k
     assert torch.equal(sh, sd.cpu()) and torch.equal(vh, vd.cpu()) and torch.equal(uh, ud.cpu())
 

@@ -1,12 +1,20 @@
 """World-size-2 CPU (gloo) tests of the N>1 path's host-side logic.
 
 The GPU path runs one process per GPU: every rank streams its own row shard,
-the small partials (Gram matrix, column sums of squares, A^T Q) are
+the small partials (packed Gram matrix, column sums of squares, A^T Q) are
 sum-allreduced, and every small core is recomputed redundantly on each rank.
-These tests replay exactly that data flow with the oracle's step functions and
-gloo allreduces, and check (a) it reproduces the single-process oracle and (b)
-replicated results are bit-identical on every rank; plus bench.py's torchrun
-launch (rank 0 prints one line, the other ranks exit 0).
+
+These tests do not re-type that data flow: each rank asks the LIBRARY for the
+exact step sequence its orchestrator (csrc/api.cu) would run on that rank
+(`tssvd_trace`, a plan-only run that makes no CUDA or NCCL call), and replays
+it token by token -- numpy for the local arithmetic (LAPACK standing in for the
+Jacobi kernels), gloo allreduces for the collectives, with the message sizes
+the trace announces.  Checks: (a) the replay reproduces the single-process
+oracle, (b) replicated results are bit-identical on every rank, (c) every
+collective's size is the one the replay needs (packed Gram w(w+1)/2, norms,
+A^T Q without pad columns), (d) the host round trips are where the design says
+(none before the end for lowrank_svd and narrow tssvd; two for wide tssvd);
+plus bench.py's torchrun launch (rank 0 prints one line, the other ranks exit 0).
 """
 import json
 import os
@@ -19,8 +27,10 @@ import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
+from parity import assert_lowrank_parity, assert_tssvd_parity
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+WP = 1e-11
 
 
 def free_port():
@@ -31,71 +41,245 @@ def free_port():
     return p
 
 
-def _worker(rank, world, port, out_q):
-    sys.path.insert(0, ROOT)
-    import oracle
+class Replay:
+    """Interprets the orchestrator's trace on one rank (numpy + gloo)."""
+
+    def __init__(self, a_local, omega=None):
+        import oracle
+
+        self.o = oracle
+        self.a = a_local
+        self.omega = omega
+        self.collectives = []   # (what, count) as announced by the trace
+        self.pending = None     # local partial awaiting its allreduce
+        self.cur = None         # the core's input matrix
+        self.dist = False
+        self.out = {}           # outputs of the last finished core
+
+    # -- collectives
+    def allreduce(self, what, count):
+        self.collectives.append((what, count))
+        if what == "m":
+            t = torch.tensor([self.a.shape[0]], dtype=torch.int64)
+            dist.all_reduce(t)
+            self.m = int(t.item())
+            return
+        # a plan-only trace carries the launch BOUNDS (a dry run's decisions keep every
+        # column), so a message is at least as large as the data the replay reduces
+        x = self.pending
+        if what == "gram":  # packed lower triangle on the wire
+            w = x.shape[0]
+            assert count >= w * (w + 1) // 2, (what, count, w)
+            il = np.tril_indices(w)
+            t = torch.from_numpy(np.ascontiguousarray(x[il]))
+            dist.all_reduce(t)
+            full = np.zeros_like(x)
+            full[il] = t.numpy()
+            self.pending = np.tril(full) + np.tril(full, -1).T
+        elif what == "norms":
+            assert count >= x.size, (what, count, x.size)
+            t = torch.from_numpy(np.ascontiguousarray(x))
+            dist.all_reduce(t)
+            self.pending = t.numpy()
+        elif what == "beta":  # n x even(l): no partial pad columns
+            n, l = x.shape
+            assert count >= n * (l + (l & 1)) and count % n == 0 and (count // n) % 2 == 0, (count, x.shape)
+            t = torch.from_numpy(np.ascontiguousarray(x))
+            dist.all_reduce(t)
+            self.pending = self.cur = t.numpy()
+        else:
+            raise AssertionError(f"unknown collective {what}")
+
+    # -- one token
+    def run(self, tok):
+        o = self.o
+        parts = tok.split(":")
+        k = parts[0]
+        if k in ("tssvd", "lowrank", "finish", "sync", "build_z", "h2d", "d2h"):
+            return
+        if k == "allreduce":
+            self.allreduce(parts[1], int(parts[2]))
+        elif k == "core":
+            self.dist = parts[1] == "sharded"
+            self.passes = int(parts[2])
+            self.x = self.cur if self.cur is not None else self.a
+            self.c = {}
+        elif k == "gram":
+            src = self.x if parts[1] == "X" else self.c["y"]
+            self.pending = src.T @ src
+            self._settle = "B" if parts[1] == "X" else "Z"
+        elif k == "eig":
+            mat = self.pending
+            _, v = o.sym_eig(mat)
+            self.c["V~" if parts[1] == "B" else "W"] = v
+        elif k == "xv":
+            yt = self.x @ self.c["V~"]
+            self.c["yt"] = yt
+            self.pending = np.sum(yt * yt, axis=0)
+        elif k == "discard":
+            s = np.sqrt(self.pending)
+            keep = o.keep_mask(s, WP)
+            if parts[1] == "1":
+                self.c.update(sig=s[keep], keep=keep)
+                self.c["y"] = self.c["yt"][:, keep] / s[keep]
+            else:
+                self.c.update(t=s[keep], keep2=keep)
+        elif k == "alg3_out":
+            c = self.c
+            order = np.argsort(-c["sig"], kind="stable")
+            c["U"] = c["y"][:, order]
+            c["S"] = c["sig"][order]
+            c["V"] = c["V~"][:, c["keep"]][:, order]
+        elif k == "qnorm":
+            qt = self.c["y"] @ self.c["W"]
+            self.c["qt"] = qt
+            self.pending = np.sum(qt * qt, axis=0)
+        elif k == "svd":
+            c = self.c
+            w = c["W"][:, c["keep2"]]
+            rmat = (c["t"][:, None] * w.T) @ (c["sig"][:, None] * c["V~"][:, c["keep"]].T)
+            p, s, vh = np.linalg.svd(rmat, full_matrices=False)
+            q = c["qt"][:, c["keep2"]] / c["t"]
+            c["U"], c["S"], c["V"] = q @ p, s, vh.T
+        elif k == "uout":
+            if "U" in self.c:  # end of a core: signs (reading R5), publish
+                u, v = o.canonical_signs(self.c["U"], self.c["V"])
+                self.out = dict(U=u, S=self.c["S"], V=v)
+                self.c = {}
+            else:  # the final product of Alg. 6 (U = Q U~[:, :k])
+                kk = min(self.k, self.final["S"].size)
+                u = self.q_last @ self.final["Ut"][:, :kk]
+                self.result = (u, self.final["S"][:kk], self.final["VA"][:, :kk])
+        elif k == "alpha":
+            qt = self.omega if self.qt is None else self.qt
+            self.cur = self.a @ qt
+        elif k == "beta":  # local A_p^T Q (the allreduce that follows, if any, sums it)
+            self.q_last = self.out["U"]
+            self.pending = self.cur = self.a.T @ self.q_last
+        elif k == "qt":
+            self.qt = self.out["U"]
+        elif k == "canon":
+            va, ut = self.o.canonical_signs(self.out["U"], self.out["V"])
+            self.final = dict(VA=va, S=self.out["S"], Ut=ut)
+        else:
+            raise AssertionError(f"unknown trace token {tok}")
+
+
+def _replay(rank, world, problem, name, m, n, trace):
     import synth
     from paper_1612_08709_b200 import shard_rows
+
+    if problem == "tssvd":
+        d = synth.config_inputs(name, m=m)
+        omega = None
+    else:
+        d = synth.config_inputs(name, m=m, n=n)
+        omega = d["Omega"]
+    r0, r1 = shard_rows(d["A"].shape[0], world, rank)
+    rp = Replay(d["A"][r0:r1], omega)
+    rp.qt = None
+    rp.k = d.get("k", 0)
+    for tok in trace:
+        rp.run(tok)
+    if problem == "tssvd":
+        res = (rp.out["U"], rp.out["S"], rp.out["V"])
+    else:
+        res = rp.result
+    return res, rp.collectives
+
+
+def _worker(rank, world, port, problem, name, m, n, out_q):
+    sys.path.insert(0, ROOT)
+    from paper_1612_08709_b200 import _lib, shard_rows
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        d = synth.config_inputs("c2", m=60_000)
-        r0, r1 = shard_rows(60_000, world, rank)
-        a = d["A"][r0:r1]
-        wp = 1e-11
+        import synth
 
-        def allreduce(x):
-            t = torch.from_numpy(np.ascontiguousarray(x))
-            dist.all_reduce(t)
-            return t.numpy()
-
-        # Alg. 4 with the GPU path's decomposition: local partial -> allreduce -> replicated core
-        b = allreduce(a.T @ a)
-        b = np.tril(b) + np.tril(b, -1).T  # symmetrise as the GPU path does after NCCL
-        _, vt = oracle.sym_eig(b)
-        yt = a @ vt
-        st = np.sqrt(allreduce(np.sum(yt * yt, axis=0)))
-        keep = oracle.keep_mask(st, wp)
-        y = yt[:, keep] / st[keep]
-        z = allreduce(y.T @ y)
-        z = np.tril(z) + np.tril(z, -1).T
-        _, w = oracle.sym_eig(z)
-        qt = y @ w
-        t = np.sqrt(allreduce(np.sum(qt * qt, axis=0)))
-        keep2 = oracle.keep_mask(t, wp)
-        q = qt[:, keep2] / t[keep2]
-        rmat = (t[keep2][:, None] * w[:, keep2].T) @ (st[keep][:, None] * vt[:, keep].T)
-        p, sig, vh = np.linalg.svd(rmat, full_matrices=False)
-        u = q @ p
-        # orthonormality of the distributed U, measured with an allreduced Gram
-        g = allreduce(u.T @ u)
-        out_q.put((rank, sig, vh, float(np.max(np.abs(g - np.eye(g.shape[0]))))))
+        cfg = synth.CONFIGS[name]
+        mm = m or cfg["m"]
+        r0, r1 = shard_rows(mm, world, rank)
+        if problem == "tssvd":
+            trace = _lib.trace("tssvd", world, r1 - r0, n or cfg["n"], wp=WP)
+        else:
+            trace = _lib.trace("lowrank", world, r1 - r0, n, cfg["l"], cfg["iters"], cfg["k"], wp=WP)
+        (u, s, v), coll = _replay(rank, world, problem, name, m, n, trace)
+        g = torch.from_numpy(np.ascontiguousarray(u.T @ u))
+        dist.all_reduce(g)  # orthonormality of the distributed U
+        out_q.put((rank, trace, coll, s, v, u, float(np.max(np.abs(g.numpy() - np.eye(g.shape[0]))))))
     finally:
         dist.destroy_process_group()
 
 
-def test_two_rank_gloo_dataflow_matches_single_process_oracle():
-    import oracle
-    import synth
-
-    world, port = 2, free_port()
+def _run_world(problem, name, m=None, n=None, world=2):
+    port = free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, problem, name, m, n, q))
+             for r in range(world)]
     for p in procs:
         p.start()
-    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda x: x[0])
+    res = sorted([q.get(timeout=600) for _ in range(world)], key=lambda x: x[0])
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    (_, s0, v0, o0), (_, s1, v1, o1) = res
+    return res
+
+
+def _syncs(trace):
+    return [t for t in trace if t.startswith("sync:")]
+
+
+@pytest.mark.parametrize("name,m,passes_syncs", [("c2", 60_000, 2), ("c1", None, 0)])
+def test_two_rank_tssvd_trace_replay(name, m, passes_syncs):
+    """tssvd (Alg. 4) on 2 ranks, replayed from the orchestrator's own trace: c2 (w = 100, the
+    eigensolver's k and the first discard's r read back: 2 syncs) and c1 (w = 10: every decision
+    on the device, no sync before the end)."""
+    import oracle
+    import synth
+
+    res = _run_world("tssvd", name, m)
+    (_, t0, c0, s0, v0, u0, o0), (_, t1, c1, s1, v1, u1, o1) = res
+    assert t0 == t1  # equal shards up to one row: identical step sequences
+    assert len(_syncs(t0)) == passes_syncs
+    whats = [w for w, _ in c0]
+    assert whats[0] == "m" and whats.count("gram") == 2 and whats.count("norms") == 2
     assert np.array_equal(s0, s1) and np.array_equal(v0, v1)  # replicated cores agree bitwise
     assert o0 <= 1e-13
-    d = synth.config_inputs("c2", m=60_000)
-    _, sr, _ = oracle.tssvd(d["A"], 1e-11, 2)
-    assert s0.size == sr.size == 55
-    assert np.max(np.abs(s0 - sr)) <= 1e-12
+    d = synth.config_inputs(name, m=m)
+    ref = oracle.tssvd(d["A"], WP, 2)
+    assert_tssvd_parity((np.vstack([u0, u1]), s0, v0), ref, passes=2, sigma_tol=1e-12)
+
+
+def test_two_rank_lowrank_trace_replay():
+    """lowrank_svd (Alg. 8) on 2 ranks from the trace: no host round trip before the end,
+    the A^T Q allreduce without pad columns (n x even(l)), replicated factors bit-identical,
+    and the single-process oracle reproduced."""
+    import oracle
+    import synth
+
+    m, n = 8_000, 1_001
+    res = _run_world("lowrank", "c3", m, n)
+    (_, t0, c0, s0, v0, u0, o0), (_, t1, c1, s1, v1, u1, o1) = res
+    assert t0 == t1 and _syncs(t0) == [] and t0[-1] == "finish"
+    cfg = synth.CONFIGS["c3"]
+    betas = [c for w, c in c0 if w == "beta"]
+    assert betas == [n * (cfg["l"] + (cfg["l"] & 1))] * (cfg["iters"] + 1)
+    assert np.array_equal(s0, s1) and np.array_equal(v0, v1)
+    assert o0 <= 1e-13
+    d = synth.config_inputs("c3", m=m, n=n)
+    ref = oracle.lowrank_svd(d["A"], d["Omega"], cfg["iters"], cfg["k"], WP)
+    assert s0.size == ref[1].size == cfg["k"]
+    assert_lowrank_parity((np.vstack([u0, u1]), s0, v0), ref, d["A"], d["x0"])
+
+
+def test_trace_single_rank_has_no_collectives():
+    from paper_1612_08709_b200 import _lib
+
+    for t in (_lib.trace("tssvd", 1, 100_000, 100), _lib.trace("lowrank", 1, 10_000, 2_000, 25, 2, 20)):
+        assert not [x for x in t if x.startswith("allreduce")]
+        assert t[-1] == "finish" or t[-1].startswith("d2h")
 
 
 def test_bench_reference_arm_under_torchrun_two_ranks():
