@@ -417,7 +417,7 @@ CoreOut core(Ctx& c, Core& b, const double* X, int64_t ldx, int64_t m_local, int
   KS(cols_to_m(b.B, w, w, k, b.M, smem_ld(k), mrows_for(w), s));
   {
     Pass t(s, TSSVD_PASS_XV, 2.0 * m_local * w * k, 8.0 * m_local * (w + k));
-    KL(launch_gemm_nn(X, ldx, m_local, w, b.M, k, U, ldu, b.npart, s));
+    KL(launch_gemm_nn(X, ldx, m_local, w, b.M, k, U, ldu, b.npart, nullptr, s));
     KL(launch_reduce_parts(b.npart, gemm_nn_grid(std::max<int64_t>(m_local, 1), k), gemm_nn_part_stride(k), k, b.nsq, s));
   }
   ++g_stats.a_passes;
@@ -447,7 +447,7 @@ CoreOut core(Ctx& c, Core& b, const double* X, int64_t ldx, int64_t m_local, int
     {
       Pass t(s, TSSVD_PASS_UOUT, 2.0 * m_local * nc * r, 8.0 * m_local * (nc + r));
       KL(launch_gemm_nn(U, ldu, m_local, nc, b.M, r, Upack ? Upack : U, Upack ? (r + 1) & ~1 : ldu,
-                        nullptr, s));
+                        nullptr, nullptr, s));
     }
     out.bound = r;
     out.slot = s1;
@@ -478,7 +478,7 @@ CoreOut core(Ctx& c, Core& b, const double* X, int64_t ldx, int64_t m_local, int
   KS(build_m1(b.Z, rb, b.idx, b.sig, d1, rb, kz, b.M, ldm_k, s));
   {
     Pass t(s, TSSVD_PASS_QNORM, 2.0 * m_local * nc * kz, 8.0 * m_local * nc);
-    KL(launch_gemm_nn(U, ldu, m_local, nc, b.M, kz, nullptr, 0, b.npart, s));
+    KL(launch_gemm_nn(U, ldu, m_local, nc, b.M, kz, nullptr, 0, b.npart, nullptr, s));
     KL(launch_reduce_parts(b.npart, gemm_nn_grid(std::max<int64_t>(m_local, 1), kz), gemm_nn_part_stride(kz), kz, b.tsq, s));
   }
   allreduce(cd, b.tsq, kz, "norms");
@@ -507,7 +507,7 @@ CoreOut core(Ctx& c, Core& b, const double* X, int64_t ldx, int64_t m_local, int
   {
     Pass t(s, TSSVD_PASS_UOUT, 2.0 * m_local * nc * rb2, 8.0 * m_local * (nc + rb2));
     KL(launch_gemm_nn(U, ldu, m_local, nc, b.M, rb2, Upack ? Upack : U, Upack ? (rb2 + 1) & ~1 : ldu,
-                      nullptr, s));
+                      nullptr, nullptr, s));
   }
   out.bound = rb2;
   out.slot = s2;
@@ -677,7 +677,7 @@ void tssvd_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, cons
 struct LrPlan {
   Core tall, small;
   int* ctl;
-  double *Qt, *Y, *Z, *tn, *Ut, *sig_tmp, *v_scr, *sig_scr, *Mfin;
+  double *Qt, *Y, *Z, *tn, *Ut, *sig_tmp, *v_scr, *sig_scr, *Mfin, *sk;
   double *a_stage, *o_stage, *u_stage, *s_stage, *vo_stage;
   int lp, ldzmax;
 };
@@ -699,6 +699,7 @@ size_t plan_lowrank(Arena& a, LrPlan& p, int64_t m_local, int n, int l, const ts
   p.sig_scr = a.get<double>(l);
   p.v_scr = a.get<double>((size_t)std::max(n, l) * l);
   p.Mfin = a.get<double>(gemm_nn_m_doubles(l, l));
+  p.sk = a.get<double>(gemm_nn_scratch_doubles(std::max<int64_t>(m_local, 1), n, l));  // alpha stream-K records
   if (o && o->host_io) {
     p.a_stage = a.get<double>((size_t)std::max<int64_t>(m_local, 1) * even(n));
     p.o_stage = a.get<double>((size_t)n * even(l));
@@ -790,7 +791,7 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
     step("alpha:%d", Lc);
     {
       Pass t(c.s, TSSVD_PASS_ALPHA, 2.0 * m_local * N * Lc, 8.0 * m_local * (N + Lc));
-      KL(launch_gemm_nn(Ad, ldad, m_local, N, p.Qt, Lc, p.Y, p.lp, nullptr, c.s));
+      KL(launch_gemm_nn(Ad, ldad, m_local, N, p.Qt, Lc, p.Y, p.lp, nullptr, p.sk, c.s));
     }
     ++g_stats.a_passes;
     // step 4: Y_j = Q_j R_j by Alg. 3 (Q_j = U, in place in Y)
@@ -806,7 +807,7 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
   step("alpha:%d", Lc);
   {
     Pass t(c.s, TSSVD_PASS_ALPHA, 2.0 * m_local * N * Lc, 8.0 * m_local * (N + Lc));
-    KL(launch_gemm_nn(Ad, ldad, m_local, N, p.Qt, Lc, p.Y, p.lp, nullptr, c.s));
+    KL(launch_gemm_nn(Ad, ldad, m_local, N, p.Qt, Lc, p.Y, p.lp, nullptr, p.sk, c.s));
   }
   ++g_stats.a_passes;
   const CoreOut o3 = core(c, p.tall, p.Y, p.lp, m_local, Lc, 2, true, p.Y, p.lp, p.sig_scr, p.v_scr, Lc, true);
@@ -822,7 +823,7 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
   KS(rows_to_m(p.Ut, Lc, o3.bound, kk, p.Mfin, smem_ld(kk), mrows_for(o3.bound), c.s));
   double* Uo = hio ? p.u_stage : U;
   const int64_t lduo = hio ? even(kk) : ldu;  // even: the GEMM stores double2 pairs
-  KL(launch_gemm_nn(p.Y, p.lp, m_local, o3.bound, p.Mfin, kk, Uo, lduo, nullptr, c.s));
+  KL(launch_gemm_nn(p.Y, p.lp, m_local, o3.bound, p.Mfin, kk, Uo, lduo, nullptr, nullptr, c.s));
   double* So = hio ? p.s_stage : sigma;
   double* Vo = hio ? p.vo_stage : V;
   const int64_t ldvo = hio ? kk : ldv;
@@ -1057,7 +1058,8 @@ int tssvd_gram(void* stream, int64_t m, int64_t n, const double* X, int64_t ldx,
 }
 
 size_t tssvd_matmul_workspace(int64_t m, int64_t k, int64_t c) {
-  return (gemm_nn_m_doubles((int)k, (int)c) + (size_t)gemm_nn_grid(std::max<int64_t>(m, 1), (int)c) * gemm_nn_part_stride((int)c) + 128) * 8;
+  return (gemm_nn_m_doubles((int)k, (int)c) + (size_t)gemm_nn_grid(std::max<int64_t>(m, 1), (int)c) * gemm_nn_part_stride((int)c) +
+          gemm_nn_scratch_doubles(m, (int)k, (int)c) + 128) * 8;
 }
 
 int tssvd_matmul(void* stream, int64_t m, int64_t k, int64_t c, const double* X, int64_t ldx,
@@ -1073,7 +1075,8 @@ int tssvd_matmul(void* stream, int64_t m, int64_t k, int64_t c, const double* X,
     double* np = Mp + ((gemm_nn_m_doubles((int)k, (int)c) + 31) & ~size_t(31));
     rows_to_m(M, ldm, (int)k, (int)c, Mp, smem_ld((int)c), mrows_for((int)k), s);
     CU(cudaGetLastError());
-    CU(launch_gemm_nn(X, ldx, m, (int)k, Mp, (int)c, Y, ldy, nsq ? np : nullptr, s));
+    double* sk = np + (size_t)gemm_nn_grid(std::max<int64_t>(m, 1), (int)c) * gemm_nn_part_stride((int)c);
+    CU(launch_gemm_nn(X, ldx, m, (int)k, Mp, (int)c, Y, ldy, nsq ? np : nullptr, sk, s));
     if (nsq)
       CU(launch_reduce_parts(np, gemm_nn_grid(std::max<int64_t>(m, 1), (int)c), gemm_nn_part_stride((int)c), c, nsq, s));
     CU(cudaStreamSynchronize(s));

@@ -30,9 +30,13 @@ cudaError_t launch_reduce_sym(const double* part, int nparts, int w, double* B, 
 // In place (Y == X, ldy == ldx) is allowed.
 int gemm_nn_grid(int64_t m, int c);
 int gemm_nn_part_stride(int c);  // doubles per CTA in norm_part (>= pad8(c))
+// scratch (nullable): gemm_nn_scratch_doubles(m, k, c) doubles enable the stream-K work split
+// (used only without norm_part; a null scratch runs the row-tile split).
 cudaError_t launch_gemm_nn(const double* X, int64_t ldx, int64_t m, int k, const double* M,
-                           int c, double* Y, int64_t ldy, double* norm_part, cudaStream_t s);
+                           int c, double* Y, int64_t ldy, double* norm_part, double* scratch,
+                           cudaStream_t s);
 size_t gemm_nn_m_doubles(int k, int c);  // size of the padded M buffer
+size_t gemm_nn_scratch_doubles(int64_t m, int k, int c);
 
 // Z (n x l, ld ldz) partials: Zp[split][n_pad x ldz] = X[rows, :n]^T * Y[rows, :l]
 // reduced over `splits` row ranges.

@@ -424,11 +424,19 @@ cudaError_t launch_reduce_parts_2d(const double* part, int np, int64_t stride, i
 // (MI * NIW <= 12 tiles, one column group: register room for 13 warps), else 8.
 __host__ __device__ constexpr int nn_cw(int mi, int niw, int wc) { return mi * niw <= 12 && wc == 1 ? 12 : 8; }
 
+// Stream-K mode (sk_rec != nullptr; only without the norm epilogue): the ntiles x kc_count
+// (tile, K-chunk) units are cut into gridDim.x contiguous, equal ranges (tile-major), so
+// every CTA streams the same number of chunks whatever ntiles mod gridDim.x is (c3 alpha:
+// 521 row tiles on 148 SMs left a 12% tail).  A tile whose chunks are split between CTAs
+// leaves partial accumulators in per-CTA records (slot 2b: the CTA's first tile, 2b + 1:
+// its last), which gemm_nn_fixup sums in CTA (= K) order and stores.
+__host__ __device__ inline int64_t sk_u0(int b, int64_t units, int grid) { return units * b / grid; }
+
 template <int MI, int NIW, int WC, int XR, int NN_CW = nn_cw(MI, NIW, WC)>
 __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
     const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tm, int64_t m, int k,
     int KC, int kc_count, int LDM, int c, double* Y, int64_t ldy, double* __restrict__ norm_part,
-    int nst) {
+    int nst, double* __restrict__ sk_rec) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int RW = NN_CW / WC;
   constexpr int R = 8 * MI * RW;
@@ -440,8 +448,22 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
   const int xs_d = R * KC, stage_d = xs_d + KC * LDM;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int64_t ntiles = ceil_div(m, R);
+  const bool sk = sk_rec != nullptr;
+  const int64_t units = ntiles * kc_count;
+  const int64_t u0 = sk ? sk_u0(blockIdx.x, units, gridDim.x) : 0;
   const int64_t mytiles = blockIdx.x < ntiles ? ceil_div(ntiles - blockIdx.x, (int64_t)gridDim.x) : 0;
-  const int64_t nsteps = mytiles * kc_count;
+  const int64_t nsteps = sk ? sk_u0(blockIdx.x + 1, units, gridDim.x) - u0 : mytiles * kc_count;
+  const int64_t first_tile = sk ? u0 / kc_count : -1;
+  // step s -> (row tile, K chunk)
+  auto unit = [&](int64_t s, int64_t& tile, int& chunk) {
+    if (sk) {
+      tile = (u0 + s) / kc_count;
+      chunk = (int)((u0 + s) % kc_count);
+    } else {
+      tile = blockIdx.x + (s / kc_count) * gridDim.x;
+      chunk = (int)(s % kc_count);
+    }
+  };
   ring_init(ring, nst, NN_CW);
 
   if (warp == NN_CW) {  // ---- producer (last warp)
@@ -450,8 +472,10 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
         const int b = (int)(s % nst);
         const int64_t u = s / nst;
         if (u > 0) mbar_wait(ring.empty(b), (uint32_t)((u - 1) & 1));
-        const int64_t tile = blockIdx.x + (s / kc_count) * gridDim.x;
-        const int k0 = (int)(s % kc_count) * KC;
+        int64_t tile;
+        int chunk;
+        unit(s, tile, chunk);
+        const int k0 = chunk * KC;
         double* xs = buf + b * stage_d;
         mbar_arrive_expect_tx(ring.full(b), (uint32_t)(stage_d * 8));
         // the X box in TMA boxes of at most 256 rows (R = 384 with 12 consumer warps)
@@ -488,12 +512,16 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
   if (norm_part && !NRM)
     for (int col = lane; col < NB * 8; col += 32) red[col] = 0.0;
 
+  bool partial = false;  // stream-K: this CTA's part of the current tile misses chunks
   for (int64_t s = 0; s < nsteps; ++s) {
     const int b = (int)(s % nst);
     mbar_wait(ring.full(b), (uint32_t)((s / nst) & 1));
     const double* xs = buf + b * stage_d + (rg * MI * 8 + g) * KC + t;
     const double* ms = buf + b * stage_d + xs_d + t * LDM + col0 + g;
-    const int kc_here = (int)(s % kc_count);
+    int64_t tile;
+    int kc_here;
+    unit(s, tile, kc_here);
+    if (s == 0 || kc_here == 0) partial = kc_here != 0;
     const int nks = min(KC / 4, (k - kc_here * KC + 3) / 4);  // k-steps holding real columns
     // (software-pipelining the fragment loads, as gemm_tn does, measured slower
     // here: 7.9 -> 9.0 ms per c3 alpha pass)
@@ -518,8 +546,31 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(ring.empty(b));
-    if (kc_here == kc_count - 1) {  // tile complete: epilogue
-      const int64_t tile = blockIdx.x + (s / kc_count) * gridDim.x;
+    if (sk && s == nsteps - 1 && kc_here != kc_count - 1) partial = true;
+    if (sk && partial && (kc_here == kc_count - 1 || s == nsteps - 1)) {
+      // stream-K partial tile: accumulators to this CTA's record (summed by gemm_nn_fixup)
+      double* rec = sk_rec + (size_t)(2 * blockIdx.x + (tile == first_tile ? 0 : 1)) * R * CP;
+#pragma unroll
+      for (int i = 0; i < MI; ++i) {
+        const int row = (rg * MI + i) * 8 + g;
+#pragma unroll
+        for (int j = 0; j < NIW; ++j) {
+          *reinterpret_cast<double2*>(rec + (size_t)row * CP + col0 + j * 8 + 2 * t) =
+              make_double2(acc[i][j][0], acc[i][j][1]);
+          acc[i][j][0] = acc[i][j][1] = 0.0;
+        }
+        if constexpr (XR > 0) {
+#pragma unroll
+          for (int x = 0; x < XR; ++x) {
+            double v = ex[i][x];
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            v += __shfl_xor_sync(0xffffffffu, v, 2);
+            ex[i][x] = 0.0;
+            if (t == x) rec[(size_t)row * CP + NIW * 8 + x] = v;
+          }
+        }
+      }
+    } else if (kc_here == kc_count - 1) {  // tile complete: epilogue
       if (norm_part && NRM) {  // rows beyond m hold zeros (TMA zero fill): no masking needed
 #pragma unroll
         for (int j = 0; j < (NRM ? NIW : 1); ++j)
@@ -611,6 +662,32 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
   }
 }
 
+// Stream-K fixup: one block per CTA boundary b >= 1 that cuts a tile t (and is the first
+// boundary inside t): the records of the CTAs covering t are summed in CTA order (= K
+// order, fixed) and the rows of t stored (columns < c, rows < m).
+__global__ void __launch_bounds__(256) gemm_nn_fixup(const double* __restrict__ rec, int R, int CP, int c,
+                                                    int64_t m, int64_t ntiles, int kc_count, int grid,
+                                                    double* Y, int64_t ldy) {
+  const int b = blockIdx.x + 1;
+  const int64_t units = ntiles * kc_count;
+  const int64_t ub = sk_u0(b, units, grid);
+  if (ub % kc_count == 0 || ub >= units) return;
+  const int64_t t = ub / kc_count;
+  if (sk_u0(b - 1, units, grid) > t * kc_count) return;  // an earlier boundary cut t already
+  int bl = b;  // last CTA covering t
+  while (bl + 1 < grid && sk_u0(bl + 1, units, grid) < (t + 1) * kc_count) ++bl;
+  for (int e = threadIdx.x; e < R * c; e += blockDim.x) {
+    const int row = e / c, col = e % c;
+    double v = 0.0;
+    for (int q = b - 1; q <= bl; ++q) {
+      const int slot = 2 * q + (sk_u0(q, units, grid) / kc_count == t ? 0 : 1);
+      v += rec[((size_t)slot * R + row) * CP + col];
+    }
+    const int64_t grow = t * R + row;
+    if (grow < m) Y[grow * ldy + col] = v;
+  }
+}
+
 // Warp grid and rows per tile from the accumulator budget (<= 24 8x8 tiles,
 // <= 16 column blocks per warp); c = 8 ni + 1 or + 2 (1 <= ni <= 4, where the
 // extra accumulators still fit without spills) puts the last one or two columns
@@ -636,9 +713,12 @@ static NnShape nn_shape(int c) {
 
 struct NnPlan {
   NnShape sh;
-  int ni, R, KC, kcc, nst, grid, ldm;
+  int ni, R, KC, kcc, nst, grid, ldm, cp;
+  bool sk;  // stream-K work split (see gemm_nn_kernel)
   size_t smem;
 };
+
+int gemm_nn_part_stride(int c);
 
 // K chunk (= 4 mod 8, <= 252) and stage count from shared memory: fewest
 // zero-filled columns, then fewest chunks, with at least 2 stages (3
@@ -669,7 +749,17 @@ static NnPlan plan_nn(int64_t m, int k, int c) {
   const size_t stage = (size_t)(p.R * p.KC + p.KC * p.ldm) * 8;
   p.nst = (int)std::max<size_t>(2, std::min<size_t>(8, budget / stage));
   p.smem = kBarBytes + (size_t)p.nst * stage + red;
-  p.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(m, p.R), dev_info().sms));
+  const int64_t ntiles = ceil_div(m, p.R);
+  p.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, dev_info().sms));
+  p.cp = gemm_nn_part_stride(c);
+  // stream-K when the row tiles keep less than 97% of the SMs busy over the waves (a
+  // ragged last wave, or fewer tiles than SMs: then it is a split-K) and K has >= 2 chunks
+  // (TSSVD_NN_SK=0/1 forces, experiments)
+  static const int force_sk = getenv("TSSVD_NN_SK") ? atoi(getenv("TSSVD_NN_SK")) : -1;
+  const int sms = dev_info().sms;
+  const double tail = (double)ceil_div(ntiles, sms) * sms / (double)ntiles - 1.0;
+  p.sk = p.kcc >= 2 && ntiles * p.kcc >= 2 * dev_info().sms && (force_sk >= 0 ? force_sk == 1 : tail > 0.03);
+  if (p.sk) p.grid = dev_info().sms;
   return p;
 }
 
@@ -683,32 +773,49 @@ int gemm_nn_part_stride(int c) {
   return (sh.niw + (sh.xr > 0)) * sh.wc * 8;
 }
 size_t gemm_nn_m_doubles(int k, int c) { return (size_t)ceil_div(k + 1, 32) * 32 * smem_ld(c); }
+size_t gemm_nn_scratch_doubles(int64_t m, int k, int c) {
+  if (c <= 0 || c > 256) return 0;
+  const NnPlan p = plan_nn(std::max<int64_t>(m, 1), std::max(k, 1), c);
+  return p.sk ? (size_t)2 * p.grid * p.R * p.cp : 0;
+}
 
 template <int MI, int NIW, int WC, int XR>
 static cudaError_t nn_go(const NnPlan& p, const CUtensorMap& tx, const CUtensorMap& tm, int64_t m,
-                         int k, int c, double* Y, int64_t ldy, double* norm_part, cudaStream_t s) {
+                         int k, int c, double* Y, int64_t ldy, double* norm_part, double* sk_rec,
+                         cudaStream_t s) {
   auto kern = gemm_nn_kernel<MI, NIW, WC, XR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
   if (e != cudaSuccess) return e;
   kern<<<p.grid, (nn_cw(MI, NIW, WC) + 1) * 32, p.smem, s>>>(tx, tm, m, k, p.KC, p.kcc, p.ldm, c, Y, ldy, norm_part,
-                                                p.nst);
+                                                p.nst, sk_rec);
+  e = cudaGetLastError();
+  if (e != cudaSuccess || !sk_rec) return e;
+  gemm_nn_fixup<<<p.grid - 1 > 0 ? p.grid - 1 : 1, 256, 0, s>>>(sk_rec, p.R, p.cp, c, m, ceil_div(m, p.R), p.kcc,
+                                                               p.grid, Y, ldy);
   return cudaGetLastError();
 }
 
 template <int NI, int XR = 0, int WCF = 0>
 static cudaError_t nn_ni_go(const NnPlan& p, const CUtensorMap& tx, const CUtensorMap& tm, int64_t m,
-                            int k, int c, double* Y, int64_t ldy, double* np, cudaStream_t s) {
+                            int k, int c, double* Y, int64_t ldy, double* np, double* sk_rec, cudaStream_t s) {
   constexpr int WC = WCF ? WCF : (NI <= 16 ? 1 : 2);
   constexpr int NIW = (NI + WC - 1) / WC;
   constexpr int MI = 24 / NIW < 1 ? 1 : (24 / NIW > 4 ? 4 : 24 / NIW);
-  return nn_go<MI, NIW, WC, XR>(p, tx, tm, m, k, c, Y, ldy, np, s);
+  return nn_go<MI, NIW, WC, XR>(p, tx, tm, m, k, c, Y, ldy, np, sk_rec, s);
 }
 
 cudaError_t launch_gemm_nn(const double* X, int64_t ldx, int64_t m, int k, const double* M,
-                           int c, double* Y, int64_t ldy, double* norm_part, cudaStream_t s) {
+                           int c, double* Y, int64_t ldy, double* norm_part, double* scratch,
+                           cudaStream_t s) {
   if (c <= 0) return cudaSuccess;
   if (c > 256) return cudaErrorInvalidValue;
-  const NnPlan p = plan_nn(std::max<int64_t>(m, 1), std::max(k, 1), c);
+  NnPlan p = plan_nn(std::max<int64_t>(m, 1), std::max(k, 1), c);
+  // stream-K needs the caller's scratch (gemm_nn_scratch_doubles) and no norm epilogue
+  double* sk_rec = p.sk && scratch && !norm_part && Y ? scratch : nullptr;
+  if (p.sk && !sk_rec) {
+    p.sk = false;
+    p.grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(std::max<int64_t>(m, 1), p.R), dev_info().sms));
+  }
   if (m <= 0 || k <= 0) {
     if (norm_part) return cudaMemsetAsync(norm_part, 0, (size_t)p.grid * gemm_nn_part_stride(c) * 8, s);
     return cudaSuccess;
@@ -719,22 +826,22 @@ cudaError_t launch_gemm_nn(const double* X, int64_t ldx, int64_t m, int k, const
   e = make_tmap(&tm, M, k, smem_ld(c), smem_ld(c), p.KC, p.ldm);
   if (e != cudaSuccess) return e;
 #define NN_XCASE(N) \
-  case N: return p.sh.xr == 1 ? nn_ni_go<N, 1>(p, tx, tm, m, k, c, Y, ldy, norm_part, s) \
-                              : nn_ni_go<N, 2>(p, tx, tm, m, k, c, Y, ldy, norm_part, s);
+  case N: return p.sh.xr == 1 ? nn_ni_go<N, 1>(p, tx, tm, m, k, c, Y, ldy, norm_part, sk_rec, s) \
+                              : nn_ni_go<N, 2>(p, tx, tm, m, k, c, Y, ldy, norm_part, sk_rec, s);
   if (p.sh.xr) switch (p.ni) {
       NN_XCASE(1) NN_XCASE(2) NN_XCASE(3) NN_XCASE(4)
       default: return cudaErrorInvalidValue;
     }
 #undef NN_XCASE
 #define NN_WCASE(N) \
-  case N: return nn_ni_go<N, 0, 2>(p, tx, tm, m, k, c, Y, ldy, norm_part, s);
+  case N: return nn_ni_go<N, 0, 2>(p, tx, tm, m, k, c, Y, ldy, norm_part, sk_rec, s);
   if (p.sh.wc == 2 && p.ni <= 16) switch (p.ni) {
       NN_WCASE(9) NN_WCASE(10) NN_WCASE(11) NN_WCASE(12) NN_WCASE(13) NN_WCASE(14) NN_WCASE(15) NN_WCASE(16)
       default: return cudaErrorInvalidValue;
     }
 #undef NN_WCASE
 #define NN_CASE(N) \
-  case N: return nn_ni_go<N>(p, tx, tm, m, k, c, Y, ldy, norm_part, s);
+  case N: return nn_ni_go<N>(p, tx, tm, m, k, c, Y, ldy, norm_part, sk_rec, s);
   switch (p.ni) {
     NN_CASE(1) NN_CASE(2) NN_CASE(3) NN_CASE(4) NN_CASE(5) NN_CASE(6) NN_CASE(7) NN_CASE(8)
     NN_CASE(9) NN_CASE(10) NN_CASE(11) NN_CASE(12) NN_CASE(13) NN_CASE(14) NN_CASE(15)

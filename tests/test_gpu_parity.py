@@ -67,6 +67,25 @@ def test_matmul_kernel_vs_numpy(m, k, c):
     assert np.allclose(nsq.cpu().numpy(), np.sum(ref * ref, axis=0), rtol=1e-12, atol=0)
 
 
+@pytest.mark.parametrize("m,k,c", [(200_000, 20_000, 25), (1_000, 20_000, 25), (5_003, 8_000, 60),
+                                   (777, 3_000, 17), (100_001, 4_000, 8)])
+def test_matmul_stream_k_vs_numpy(m, k, c):
+    """Y = X M without the norm epilogue and with a large K: the stream-K work split (equal
+    (row tile, K chunk) ranges per CTA; split tiles summed in K order by the fixup kernel),
+    from a ragged last wave (c3's alpha shape, 521 tiles on 148 SMs) to a pure split-K
+    (fewer tiles than SMs, up to ~50 CTAs per tile)."""
+    rng = np.random.default_rng(m + k + c)
+    X = torch.from_numpy(rng.standard_normal((m, k))).to(DEV)
+    mm = rng.standard_normal((k, c))
+    y = tk.matmul(X, to_dev(mm)).cpu().numpy()
+    xr = X.cpu().numpy()
+    ref = xr @ mm
+    scale = np.abs(xr) @ np.abs(mm)
+    assert np.all(np.abs(y - ref) <= 1e-14 * k * scale + 1e-300)
+    y2 = tk.matmul(X, to_dev(mm)).cpu().numpy()
+    assert np.array_equal(y, y2)  # fixed-order split sums: deterministic
+
+
 def test_matmul_in_place():
     rng = np.random.default_rng(3)
     x = rng.standard_normal((10_000, 100))
@@ -528,9 +547,13 @@ def test_lowrank_c5_full_size_properties():
     iterations) against sigma_{k+1}."""
     import math
 
+    import gc
+
+    gc.collect()
+    torch.cuda.empty_cache()  # earlier tests' cached blocks (c3's 32 GB A) back to the driver
     free, _ = torch.cuda.mem_get_info()
     m, n, r, k, l, iters = 500_000, 40_000, 100, 50, 60, 4
-    if free < 8 * m * n + (12 << 30):
+    if free < 8 * m * n + (4 << 30):
         pytest.skip("not enough device memory for c5 on one GPU")
     f64 = torch.float64
     g = torch.Generator(device=DEV).manual_seed(5)
