@@ -67,6 +67,10 @@ class Clocks:
         self.proc = None
         self.path = os.path.join("/tmp", f"bench_clocks_{os.getpid()}.csv")
 
+    # The sampler is started BEFORE the warm-up steps: nvidia-smi's NVML start-up stalls the
+    # GPU for tens of ms (measured r2: a c3 line of 54.5 ms/step when it started right at the
+    # timed region, 46-47 ms/step with it running), so only its steady-state samples fall in
+    # the timed window [mark_begin, mark_end], and only those are reported.
     def start(self):
         try:
             self.proc = subprocess.Popen(
@@ -77,15 +81,31 @@ class Clocks:
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+        self.t_begin = self.t_end = None
+
+    def mark_begin(self):
+        self.n_begin = self._count()
+
+    def mark_end(self):
+        time.sleep(0.25)
+        self.n_end = self._count()
+
+    def _count(self):
+        try:
+            return sum(1 for _ in open(self.path))
+        except OSError:
+            return 0
 
     def stop(self):
         if not self.proc:
             return None
-        time.sleep(0.25)
         self.proc.terminate()
         self.proc.wait()
         rows = []
-        for line in open(self.path):
+        lines = open(self.path).read().splitlines()
+        nb, ne = getattr(self, "n_begin", 0), getattr(self, "n_end", len(lines))
+        window = lines[nb:ne] if ne > nb else lines[nb:] or lines
+        for line in window:
             f = [x.strip() for x in line.split(",")]
             if len(f) >= 7:
                 try:
@@ -240,14 +260,15 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
+    clocks = Clocks(local_rank)
+    if not args.no_clocks:
+        clocks.start()
     for _ in range(args.warmup):
         step()
     st = _lib.last_stats()
     launches = st["kernel_launches"]
     barrier()
-    clocks = Clocks(local_rank)
-    if not args.no_clocks:
-        clocks.start()
+    clocks.mark_begin()
     _lib.set_pass_timing(True)
     pass_ms = {}
     pass_flops = {}
@@ -265,6 +286,7 @@ def run_ours(args, rank, world, local_rank):
             pass_bytes.append(p["bytes"])
     e1.record(stream)
     barrier()
+    clocks.mark_end()
     _lib.set_pass_timing(False)
     ck = clocks.stop()
     t = e0.elapsed_time(e1) / args.steps  # ms per step on this rank

@@ -60,6 +60,22 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+// L2 promotion (the granule in which an L2 miss of the TMA engine is filled from
+// DRAM): 256 B when a box row is a whole contiguous matrix row; when it is only a slice
+// of a longer row (the first nc columns of Y~ inside U's ld = n rows) a 256-B fill
+// drags in neighbour bytes no one reads (ncu r1: 1.38x DRAM traffic for the Gram of
+// Y~), so those use 64 B.  TSSVD_L2PROMO = 0/64/128/256 forces one (experiments).
+static CUtensorMapL2promotion l2_promotion(int64_t cols, int64_t ld, int box_cols) {
+  static const int force = getenv("TSSVD_L2PROMO") ? atoi(getenv("TSSVD_L2PROMO")) : -1;
+  const int v = force >= 0 ? force : (cols == ld || box_cols < cols ? 256 : 64);
+  switch (v) {
+    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    case 64: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 128: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
+}
+
 // Row-major FP64 matrix (rows x cols, leading dimension ld doubles) as a 2-D
 // tensor map with boxes of box_rows x box_cols (box_cols may exceed cols:
 // the excess is zero-filled).
@@ -76,7 +92,7 @@ static cudaError_t make_tmap(CUtensorMap* map, const double* base, int64_t rows,
   const cuuint32_t es[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
                   es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  l2_promotion(cols, ld, box_cols), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
@@ -525,24 +541,28 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
     const int nks = min(KC / 4, (k - kc_here * KC + 3) / 4);  // k-steps holding real columns
     // (software-pipelining the fragment loads, as gemm_tn does, measured slower
     // here: 7.9 -> 9.0 ms per c3 alpha pass)
+    // Every fragment of a k-step is loaded (into its own register) before the first DMMA:
+    // with the B fragment loaded inside the column loop ptxas reused ONE register for all
+    // of them, so each column block's LDS waited for the previous DMMAs to read it and the
+    // next DMMA for the LDS (ncu r2, c3 alpha: the top stall, tensor pipe 75% active).
     for (int kk = 0; kk < nks; ++kk) {
-      double a[MI];
+      double a[MI], bfr[NIW], mv[XR > 0 ? XR : 1];
+#pragma unroll
+      for (int j = 0; j < NIW; ++j) bfr[j] = ms[kk * 4 * LDM + j * 8];
 #pragma unroll
       for (int i = 0; i < MI; ++i) a[i] = xs[i * 8 * KC + kk * 4];
+      if constexpr (XR > 0)  // M[4kk + t][8 NIW + x]: one broadcast load per t
 #pragma unroll
-      for (int j = 0; j < NIW; ++j) {
-        const double bf = ms[kk * 4 * LDM + j * 8];
+        for (int x = 0; x < XR; ++x) mv[x] = ms[kk * 4 * LDM - g + NIW * 8 + x];
 #pragma unroll
-        for (int i = 0; i < MI; ++i) dmma(acc[i][j], a[i], bf);
-      }
-      if constexpr (XR > 0) {  // M[4kk + t][8 NIW + x]: one broadcast load per t
+      for (int j = 0; j < NIW; ++j)
 #pragma unroll
-        for (int x = 0; x < XR; ++x) {
-          const double mv = ms[kk * 4 * LDM - g + NIW * 8 + x];
+        for (int i = 0; i < MI; ++i) dmma(acc[i][j], a[i], bfr[j]);
+      if constexpr (XR > 0)
 #pragma unroll
-          for (int i = 0; i < MI; ++i) ex[i][x] = fma(a[i], mv, ex[i][x]);
-        }
-      }
+        for (int x = 0; x < XR; ++x)
+#pragma unroll
+          for (int i = 0; i < MI; ++i) ex[i][x] = fma(a[i], mv[x], ex[i][x]);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(ring.empty(b));
@@ -744,7 +764,7 @@ static NnPlan plan_nn(int64_t m, int k, int c) {
     if (score < best) best = score, p.KC = kc;
   }
   static const int force_kc = getenv("TSSVD_NN_KC") ? atoi(getenv("TSSVD_NN_KC")) : 0;  // experiments
-  if (force_kc >= 28 && force_kc % 8 == 4) p.KC = force_kc;
+  if (force_kc >= 12 && force_kc % 8 == 4) p.KC = force_kc;
   p.kcc = (int)ceil_div(k, p.KC);
   const size_t stage = (size_t)(p.R * p.KC + p.KC * p.ldm) * 8;
   p.nst = (int)std::max<size_t>(2, std::min<size_t>(8, budget / stage));
