@@ -110,6 +110,8 @@ def lib() -> ctypes.CDLL:
                 raise RuntimeError(f"CUDA extension not built: {LIB_PATH}")
             handle = ctypes.CDLL(LIB_PATH)
             for name, res, args in SIGNATURES:
+                if _LIB_OVERRIDE and not hasattr(handle, name):
+                    continue  # an older A/B build may lack newer entry points
                 f = getattr(handle, name)
                 f.restype = res
                 f.argtypes = args

@@ -44,19 +44,23 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defines: tuple[str, ...] = ()) -> str:
+    """Compile every csrc/*.cu and link the library (out: another path, e.g. an A/B variant
+    built with extra -D defines; loaded through TSSVD_LIB)."""
+    lib_out = out or LIB
+    if not force and not out and not needs_build():
         return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
+    os.makedirs(os.path.dirname(lib_out), exist_ok=True)
     inc, lib = nccl_dirs()
     nvcc = os.environ.get("NVCC", "nvcc")
     objs = []
     procs = []
     for src in sources():
-        obj = os.path.join(LIBDIR, os.path.basename(src) + ".o")
+        obj = os.path.join(os.path.dirname(lib_out), os.path.basename(src) + (".ab" if out else "") + ".o")
         cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-Xptxas", "-warn-spills", "-I", os.path.join(ROOT, "include"), "-I", inc,
-               "-c", src, "-o", obj]
+               *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
@@ -67,15 +71,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + out)
         if verbose or "spill" in out.lower() and "0 bytes spill" not in out:
             sys.stdout.write(out)
-    tmp = LIB + ".tmp"
+    tmp = lib_out + ".tmp"
     cmd = [nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-L", lib, "-l:libnccl.so.2",
            "-Xlinker", "-rpath=" + lib, "-lcudart"]
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib_out)
     for o in objs:
         os.remove(o)
-    return LIB
+    return lib_out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-v", action="store_true")
+    ap.add_argument("--out", default=None, help="A/B variant library path")
+    ap.add_argument("-D", action="append", default=[], help="extra preprocessor define")
+    a = ap.parse_args()
+    print(build(force=a.force, verbose=a.v, out=a.out, defines=tuple(a.D)))

@@ -545,6 +545,27 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
     // with the B fragment loaded inside the column loop ptxas reused ONE register for all
     // of them, so each column block's LDS waited for the previous DMMAs to read it and the
     // next DMMA for the LDS (ncu r2, c3 alpha: the top stall, tensor pipe 75% active).
+#ifdef NN_OLD_LOOP
+    for (int kk = 0; kk < nks; ++kk) {
+      double a[MI];
+#pragma unroll
+      for (int i = 0; i < MI; ++i) a[i] = xs[i * 8 * KC + kk * 4];
+#pragma unroll
+      for (int j = 0; j < NIW; ++j) {
+        const double bf = ms[kk * 4 * LDM + j * 8];
+#pragma unroll
+        for (int i = 0; i < MI; ++i) dmma(acc[i][j], a[i], bf);
+      }
+      if constexpr (XR > 0) {
+#pragma unroll
+        for (int x = 0; x < XR; ++x) {
+          const double mv = ms[kk * 4 * LDM - g + NIW * 8 + x];
+#pragma unroll
+          for (int i = 0; i < MI; ++i) ex[i][x] = fma(a[i], mv, ex[i][x]);
+        }
+      }
+    }
+#else
     for (int kk = 0; kk < nks; ++kk) {
       double a[MI], bfr[NIW], mv[XR > 0 ? XR : 1];
 #pragma unroll
@@ -564,6 +585,7 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
 #pragma unroll
           for (int i = 0; i < MI; ++i) ex[i][x] = fma(a[i], mv[x], ex[i][x]);
     }
+#endif
     __syncwarp();
     if (lane == 0) mbar_arrive(ring.empty(b));
     if (sk && s == nsteps - 1 && kc_here != kc_count - 1) partial = true;

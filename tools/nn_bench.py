@@ -18,17 +18,18 @@ ld = int(sys.argv[5]) if len(sys.argv) > 5 else None
 g = torch.Generator(device="cuda").manual_seed(0)
 f = torch.float64
 if kind == "nn":
-    X = torch.randn(a, b, device="cuda", dtype=f, generator=g)
+    X = torch.randn(a, max(ld or 0, b + (b & 1)), device="cuda", dtype=f, generator=g)[:, :b]
     M = torch.randn(b, c, device="cuda", dtype=f, generator=g)
-    fn = lambda: tk.matmul(X, M)  # noqa: E731
+    norms = os.environ.get("NORMS") == "1"
+    fn = lambda: tk.matmul(X, M, norms=norms)  # noqa: E731
     flops = 2.0 * a * b * c
 elif kind == "tn":
     X = torch.randn(a, b, device="cuda", dtype=f, generator=g)
     Y = torch.randn(a, c + (c & 1), device="cuda", dtype=f, generator=g)
     fn = lambda: tk.matmul_tn(X, Y, c)  # noqa: E731
     flops = 2.0 * a * b * c
-else:
-    X = torch.randn(a, ld or b, device="cuda", dtype=f, generator=g)[:, :b]
+else:  # gram M W LD
+    X = torch.randn(a, max(c, b), device="cuda", dtype=f, generator=g)[:, :b]
     fn = lambda: tk.gram(X)  # noqa: E731
     flops = 1.0 * a * b * (b + 1)
 for _ in range(3):
