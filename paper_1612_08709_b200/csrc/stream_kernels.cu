@@ -448,7 +448,7 @@ __host__ __device__ constexpr int nn_cw(int mi, int niw, int wc) { return mi * n
 // its last), which gemm_nn_fixup sums in CTA (= K) order and stores.
 __host__ __device__ inline int64_t sk_u0(int b, int64_t units, int grid) { return units * b / grid; }
 
-template <int MI, int NIW, int WC, int XR, int NN_CW = nn_cw(MI, NIW, WC)>
+template <int MI, int NIW, int WC, int XR, bool SK, int NN_CW = nn_cw(MI, NIW, WC)>
 __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
     const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tm, int64_t m, int k,
     int KC, int kc_count, int LDM, int c, double* Y, int64_t ldy, double* __restrict__ norm_part,
@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
   const int xs_d = R * KC, stage_d = xs_d + KC * LDM;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int64_t ntiles = ceil_div(m, R);
-  const bool sk = sk_rec != nullptr;
+  constexpr bool sk = SK;
   const int64_t units = ntiles * kc_count;
   const int64_t u0 = sk ? sk_u0(blockIdx.x, units, gridDim.x) : 0;
   const int64_t mytiles = blockIdx.x < ntiles ? ceil_div(ntiles - blockIdx.x, (int64_t)gridDim.x) : 0;
@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
   const int64_t first_tile = sk ? u0 / kc_count : -1;
   // step s -> (row tile, K chunk)
   auto unit = [&](int64_t s, int64_t& tile, int& chunk) {
-    if (sk) {
+    if constexpr (SK) {
       tile = (u0 + s) / kc_count;
       chunk = (int)((u0 + s) % kc_count);
     } else {
@@ -534,19 +534,21 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
     mbar_wait(ring.full(b), (uint32_t)((s / nst) & 1));
     const double* xs = buf + b * stage_d + (rg * MI * 8 + g) * KC + t;
     const double* ms = buf + b * stage_d + xs_d + t * LDM + col0 + g;
-    int64_t tile;
+    int64_t tile = 0;
     int kc_here;
-    unit(s, tile, kc_here);
-    if (s == 0 || kc_here == 0) partial = kc_here != 0;
+    if constexpr (SK) {
+      unit(s, tile, kc_here);
+      if (s == 0 || kc_here == 0) partial = kc_here != 0;
+    } else {
+      kc_here = (int)(s % kc_count);
+    }
     const int nks = min(KC / 4, (k - kc_here * KC + 3) / 4);  // k-steps holding real columns
     // (software-pipelining the fragment loads, as gemm_tn does, measured slower
-    // here: 7.9 -> 9.0 ms per c3 alpha pass)
-    // Every fragment of a k-step is loaded (into its own register) before the first DMMA:
-    // with the B fragment loaded inside the column loop ptxas reused ONE register for all
-    // of them, so each column block's LDS waited for the previous DMMAs to read it and the
-    // next DMMA for the LDS (ncu r2, c3 alpha: the top stall, tensor pipe 75% active).
-#ifdef NN_OLD_LOOP
-    for (int kk = 0; kk < nks; ++kk) {
+    // here: 7.9 -> 9.0 ms per c3 alpha pass.)  SK: the fragments of a k-step are loaded
+    // before its first DMMA (c3 alpha 7.2 -> 6.9 ms); the same source order made the
+    // row-tile passes slower (c2 A V~ 1.06 -> 1.18 ms), so they keep the per-column-block
+    // loads (measured r2, tools/nn_bench.py).
+    if constexpr (!SK) for (int kk = 0; kk < nks; ++kk) {
       double a[MI];
 #pragma unroll
       for (int i = 0; i < MI; ++i) a[i] = xs[i * 8 * KC + kk * 4];
@@ -565,8 +567,7 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
         }
       }
     }
-#else
-    for (int kk = 0; kk < nks; ++kk) {
+    else for (int kk = 0; kk < nks; ++kk) {
       double a[MI], bfr[NIW], mv[XR > 0 ? XR : 1];
 #pragma unroll
       for (int j = 0; j < NIW; ++j) bfr[j] = ms[kk * 4 * LDM + j * 8];
@@ -585,11 +586,11 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
 #pragma unroll
           for (int i = 0; i < MI; ++i) ex[i][x] = fma(a[i], mv[x], ex[i][x]);
     }
-#endif
     __syncwarp();
     if (lane == 0) mbar_arrive(ring.empty(b));
-    if (sk && s == nsteps - 1 && kc_here != kc_count - 1) partial = true;
-    if (sk && partial && (kc_here == kc_count - 1 || s == nsteps - 1)) {
+    if constexpr (SK)
+      if (s == nsteps - 1 && kc_here != kc_count - 1) partial = true;
+    if (SK && partial && (kc_here == kc_count - 1 || s == nsteps - 1)) {
       // stream-K partial tile: accumulators to this CTA's record (summed by gemm_nn_fixup)
       double* rec = sk_rec + (size_t)(2 * blockIdx.x + (tile == first_tile ? 0 : 1)) * R * CP;
 #pragma unroll
@@ -613,6 +614,7 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
         }
       }
     } else if (kc_here == kc_count - 1) {  // tile complete: epilogue
+      if constexpr (!SK) tile = blockIdx.x + (s / kc_count) * gridDim.x;
       if (norm_part && NRM) {  // rows beyond m hold zeros (TMA zero fill): no masking needed
 #pragma unroll
         for (int j = 0; j < (NRM ? NIW : 1); ++j)
@@ -750,6 +752,10 @@ static NnShape nn_shape(int c) {
   sh.wc = sh.ni < wc2_from || sh.xr ? 1 : 2;
   sh.niw = (sh.ni + sh.wc - 1) / sh.wc;
   sh.mi = std::max(1, std::min(4, 24 / sh.niw));
+  // remainder-column shapes (c = 8j + 1/2, j <= 4): TSSVD_NN_MI = 2/3/4 row blocks per warp
+  // (R = 96 MI rows per tile; experiments)
+  static const int force_mi = getenv("TSSVD_NN_MI") ? atoi(getenv("TSSVD_NN_MI")) : 0;
+  if (sh.xr && force_mi >= 2 && force_mi <= 4) sh.mi = force_mi;
   return sh;
 }
 
@@ -825,7 +831,7 @@ template <int MI, int NIW, int WC, int XR>
 static cudaError_t nn_go(const NnPlan& p, const CUtensorMap& tx, const CUtensorMap& tm, int64_t m,
                          int k, int c, double* Y, int64_t ldy, double* norm_part, double* sk_rec,
                          cudaStream_t s) {
-  auto kern = gemm_nn_kernel<MI, NIW, WC, XR>;
+  auto kern = sk_rec ? gemm_nn_kernel<MI, NIW, WC, XR, true> : gemm_nn_kernel<MI, NIW, WC, XR, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
   if (e != cudaSuccess) return e;
   kern<<<p.grid, (nn_cw(MI, NIW, WC) + 1) * 32, p.smem, s>>>(tx, tm, m, k, p.KC, p.kcc, p.ldm, c, Y, ldy, norm_part,
@@ -843,6 +849,10 @@ static cudaError_t nn_ni_go(const NnPlan& p, const CUtensorMap& tx, const CUtens
   constexpr int WC = WCF ? WCF : (NI <= 16 ? 1 : 2);
   constexpr int NIW = (NI + WC - 1) / WC;
   constexpr int MI = 24 / NIW < 1 ? 1 : (24 / NIW > 4 ? 4 : 24 / NIW);
+  if constexpr (XR > 0 && MI == 4) {  // remainder shapes: the planner's row blocks per warp
+    if (p.sh.mi == 2) return nn_go<2, NIW, WC, XR>(p, tx, tm, m, k, c, Y, ldy, np, sk_rec, s);
+    if (p.sh.mi == 3) return nn_go<3, NIW, WC, XR>(p, tx, tm, m, k, c, Y, ldy, np, sk_rec, s);
+  }
   return nn_go<MI, NIW, WC, XR>(p, tx, tm, m, k, c, Y, ldy, np, sk_rec, s);
 }
 
