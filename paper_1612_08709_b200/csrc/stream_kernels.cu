@@ -712,23 +712,28 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
 __global__ void __launch_bounds__(256) gemm_nn_fixup(const double* __restrict__ rec, int R, int CP, int c,
                                                     int64_t m, int64_t ntiles, int kc_count, int grid,
                                                     double* Y, int64_t ldy) {
+  __shared__ int s_slot[1024];  // record slots of the CTAs covering the tile, in CTA (= K) order
+  __shared__ int s_n;
   const int b = blockIdx.x + 1;
   const int64_t units = ntiles * kc_count;
   const int64_t ub = sk_u0(b, units, grid);
   if (ub % kc_count == 0 || ub >= units) return;
   const int64_t t = ub / kc_count;
   if (sk_u0(b - 1, units, grid) > t * kc_count) return;  // an earlier boundary cut t already
-  int bl = b;  // last CTA covering t
-  while (bl + 1 < grid && sk_u0(bl + 1, units, grid) < (t + 1) * kc_count) ++bl;
-  for (int e = threadIdx.x; e < R * c; e += blockDim.x) {
+  if (threadIdx.x == 0) {
+    int n = 0;
+    for (int q = b - 1; q < grid && n < 1024 && sk_u0(q, units, grid) < (t + 1) * kc_count; ++q)
+      s_slot[n++] = 2 * q + (sk_u0(q, units, grid) / kc_count == t ? 0 : 1);
+    s_n = n;
+  }
+  __syncthreads();
+  const int nq = s_n;
+  const int64_t rows = min((int64_t)R, m - t * R);
+  for (int e = threadIdx.x; e < rows * c; e += blockDim.x) {
     const int row = e / c, col = e % c;
     double v = 0.0;
-    for (int q = b - 1; q <= bl; ++q) {
-      const int slot = 2 * q + (sk_u0(q, units, grid) / kc_count == t ? 0 : 1);
-      v += rec[((size_t)slot * R + row) * CP + col];
-    }
-    const int64_t grow = t * R + row;
-    if (grow < m) Y[grow * ldy + col] = v;
+    for (int q = 0; q < nq; ++q) v += rec[((size_t)s_slot[q] * R + row) * CP + col];
+    Y[(t * R + row) * ldy + col] = v;
   }
 }
 
