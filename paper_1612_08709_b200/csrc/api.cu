@@ -1105,12 +1105,15 @@ int tssvd_matmul_tn(void* stream, int64_t m, int64_t n, int64_t l, const double*
   });
 }
 
-size_t tssvd_sym_eig_workspace(int64_t n) { return ((size_t)n * n + 64) * 8; }
+size_t tssvd_sym_eig_workspace(int64_t n) {
+  const size_t wide = n > 256 && n <= 2048 ? jacobi_wide_workspace((int)n, (int)n) : 0;
+  return ((size_t)n * n + 64 + wide) * 8;
+}
 
 int tssvd_sym_eig(void* stream, int64_t n, const double* B, int64_t ldb, double* lambda, double* Vt,
                   int64_t ldv, int max_sweeps, int* sweeps, void* ws, size_t wsb) {
   return guarded([&] {
-    if (n < 1 || n > 256 || ldb < n || ldv < n) fail(TSSVD_EINVAL, "bad sym_eig arguments (1 <= n <= 256, ldb, ldv >= n)");
+    if (n < 1 || n > 2048 || ldb < n || ldv < n) fail(TSSVD_EINVAL, "bad sym_eig arguments (1 <= n <= 2048, ldb, ldv >= n)");
     if (wsb < tssvd_sym_eig_workspace(n)) fail(TSSVD_ENOMEM, "sym_eig workspace too small");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     double* vecs = static_cast<double*>(ws);
@@ -1119,8 +1122,12 @@ int tssvd_sym_eig(void* stream, int64_t n, const double* B, int64_t ldb, double*
     fill(lambda, n, 0.0, s);
     CU(cudaGetLastError());
     // no truncation beyond the noise floor: trunc = eps
-    CU(launch_jacobi_eig(B, (int)ldb, (int)n, jacobi_tol((int)n), kEps, max_sweeps,
-                         vecs, (int)n, lambda, info, s));
+    if (n <= 256)
+      CU(launch_jacobi_eig(B, (int)ldb, (int)n, jacobi_tol((int)n), kEps, max_sweeps,
+                           vecs, (int)n, lambda, info, s));
+    else  // the cooperative multi-CTA solver (jacobi_wide.cu)
+      CU(launch_jacobi_eig_wide(B, (int)ldb, (int)n, jacobi_tol((int)n), kEps, max_sweeps, vecs, (int)n, lambda,
+                                info, reinterpret_cast<double*>(info + 64), s));
     copy2d(vecs, n, Vt, ldv, n, (int)n, s);  // eigenvector j (contiguous) -> row j of Vt
     CU(cudaGetLastError());
     int h[3];

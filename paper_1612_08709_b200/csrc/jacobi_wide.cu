@@ -1,0 +1,527 @@
+// Wide small cores (256 < n <= 2048): the eigendecomposition / SVD steps of Alg. 3/4
+// for the paper's own n = 2000 workloads
+// (Tables 3-5, 19-21), which the one-CTA / one-cluster solver of jacobi.cu cannot hold
+// (a 2000 x 2000 Gram is 32 MB; a cluster has <= 3.6 MB of shared memory).
+//
+// Same method as jacobi.cu, spread over the whole GPU:
+//   1. diagonally pivoted Cholesky B = X X^T, truncated at trunc * max_i B_ii (reading R13),
+//      LEFT-looking: pivot k needs column p of the Schur complement,
+//        S[:, p] = B[:, p] - X[:, :k] X[p, :k]^T,
+//      a GEMV over the rows, which are dealt to all CTAs of a cooperative grid; one grid
+//      barrier per pivot (the argmax candidates of the CTAs are exchanged through global
+//      memory, double-buffered, and every CTA takes the same decision in the same order);
+//   2. one-sided BLOCK Jacobi on the K columns of X (column blocks of 16; the circle ordering
+//      over blocks; one job = one block pair = 32 columns): the 32 x 32 Gram of the pair by
+//      DMMA over the dot rows, one sweep of two-sided Jacobi on that Gram in shared memory
+//      accumulating W (32 x 32), then Y <- Y W over all rows by DMMA, in place.  A sweep with
+//      no pair above the rotation threshold ends the solve.  (Simulated on the paper's
+//      n = 2000 Gram, K = 731: 8 block sweeps + 1 check, the same count as full inner
+//      solves, eigenvalues within 4e-13 lambda_1 of LAPACK.)
+//   3. norms, descending order (ties by index), normalised output columns.
+// SVD mode skips 1: the columns are given (K = T W^T Sigma~ with an identity accumulator
+// appended, as in jacobi.cu) and only the first `dot` rows enter the Gram.
+// Every reduction has a fixed order: bit-identical results on every rank.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace tsk {
+
+static constexpr int WT = 512;   // threads per CTA
+static constexpr int WBS = 16;   // columns per block
+static constexpr int WPC = 32;   // columns per job (a block pair)
+static constexpr int WCH = 64;   // rows per streamed chunk
+static constexpr int WLD = 36;   // smem row stride of a chunk (= 4 mod 8: conflict-free fragments)
+
+__device__ __forceinline__ double rsqrt_nr_w(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double e = fma(-x * y, y, 1.0);
+    y = fma(0.5 * y, e, y);
+  }
+  return y;
+}
+
+// The rotation of jacobi.cu (jac_rot): orthogonalises columns with Gram [[al, ga], [ga, be]],
+// x_p' = c x_p - s x_q, x_q' = s x_p + c x_q; false when already orthogonal to tolerance.
+__device__ __forceinline__ bool wide_rot(double al, double be, double ga, double tol2, double skip2, double& c,
+                                         double& sn) {
+  if (!(ga != 0.0 && ga * ga > tol2 * al * be && fmax(al, be) > skip2)) return false;
+  double d = be - al, g2 = ga + ga;
+  const double big = fmax(fabs(d), fabs(g2));
+  const int ex = (int)((__double_as_longlong(big) >> 52) & 0x7ff);
+  const double sc = __longlong_as_double((long long)(2046 - ex) << 52);
+  d *= sc;
+  g2 *= sc;
+  const double w = fma(d, d, g2 * g2);
+  const double y = rsqrt_nr_w(w);
+  const double root = w * y;
+  const double q = fabs(d) + root;
+  const double u = q * (0.5 * y);
+  const double v = (root + root) * q;
+  c = u * rsqrt_nr_w(u);
+  sn = (d >= 0.0 ? g2 : -g2) * rsqrt_nr_w(v);
+  return true;
+}
+
+// ------------------------------------------------------ 1. pivoted Cholesky --
+struct PcholArgs {
+  const double* B;
+  int ldb, n;
+  double trunc;
+  double* X;       // row-major n x n capacity (ld n): X[i][k]
+  double* cval;    // [2][grid] candidate values
+  int* cidx;       // [2][grid] candidate rows
+  int* info;       // info[2] = K, info[6] = non-finite
+  int* K_out;      // device K (for the later launches)
+};
+
+__global__ void __launch_bounds__(WT, 1) wide_pchol_kernel(const PcholArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double wsm[];
+  const int n = a.n, G = gridDim.x, tid = threadIdx.x;
+  const int rpc = (n + G - 1) / G;
+  const int r0 = blockIdx.x * rpc, r1 = min(n, r0 + rpc);
+  const int nr = max(0, r1 - r0);
+  double* xp = wsm;              // [n] pivot row X[p][0..k)
+  double* dl = xp + n;           // [rpc] remaining diagonal of the own rows
+  int* pv = reinterpret_cast<int*>(dl + rpc);  // [rpc] pivoted flags
+  __shared__ double s_v[WT / 32];
+  __shared__ int s_i[WT / 32];
+  for (int r = tid; r < nr; r += WT) {
+    const double d = a.B[(size_t)(r0 + r) * a.ldb + r0 + r];
+    dl[r] = isnan(d) ? INFINITY : d;
+    pv[r] = 0;
+  }
+  __syncthreads();
+  const int warp = tid >> 5, lane = tid & 31;
+  // rows of this CTA are handled by groups of 16 lanes: group gi -> row r = gi, gi + 32, ...
+  const int gi = tid >> 4, gl = tid & 15;
+  double tabs = 0.0;
+  bool nonfinite = false;
+  int k = 0;
+  for (; k < n; ++k) {
+    // local argmax over unpivoted own rows (ties -> lowest row)
+    double bv = -1.0;
+    int bi = -1;
+    for (int r = tid; r < nr; r += WT)
+      if (!pv[r] && (bi < 0 || dl[r] > bv)) bv = dl[r], bi = r0 + r;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) bv = ov, bi = oi;
+    }
+    if (lane == 0) s_v[warp] = bv, s_i[warp] = bi;
+    __syncthreads();
+    if (tid == 0) {
+      double v = -1.0;
+      int i = -1;
+      for (int w = 0; w < WT / 32; ++w)
+        if (s_i[w] >= 0 && (i < 0 || s_v[w] > v || (s_v[w] == v && s_i[w] < i))) v = s_v[w], i = s_i[w];
+      a.cval[(k & 1) * G + blockIdx.x] = v;
+      a.cidx[(k & 1) * G + blockIdx.x] = i;
+    }
+    grid.sync();
+    // every CTA: the global argmax (a total order: value desc, row asc -- the same result
+    // whatever the reduction order), by warp 0, broadcast through shared memory
+    if (warp == 0) {
+      double v = -1.0;
+      int i = -1;
+      for (int c = lane; c < G; c += 32) {
+        const double cv = __ldcg(a.cval + (k & 1) * G + c);
+        const int ci = __ldcg(a.cidx + (k & 1) * G + c);
+        if (ci >= 0 && (i < 0 || cv > v || (cv == v && ci < i))) v = cv, i = ci;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, i, o);
+        if (oi >= 0 && (i < 0 || ov > v || (ov == v && oi < i))) v = ov, i = oi;
+      }
+      if (lane == 0) s_v[0] = v, s_i[0] = i;
+    }
+    __syncthreads();
+    const double dp = s_v[0];
+    const int p = s_i[0];
+    __syncthreads();  // s_v / s_i are reused by the next argmax
+    if (k == 0) {
+      nonfinite = !(dp < INFINITY);
+      tabs = a.trunc * dp;
+    }
+    if (nonfinite || p < 0 || !(dp > tabs)) break;
+    // stage row p of X (columns < k), written by its owner before the barrier
+    for (int j = tid; j < k; j += WT) xp[j] = __ldcg(a.X + (size_t)p * n + j);
+    __syncthreads();
+    const double rsq = rsqrt_nr_w(dp);
+    // column k of X on the own rows: (B[i][p] - X[i, :k] . X[p, :k]) / sqrt(dp); 16 lanes
+    // per row (a uniform trip count, so every shuffle has the full warp)
+    for (int base = 0; base < nr; base += WT / 16) {
+      const int r = base + gi;
+      const bool has = r < nr;
+      const int i = r0 + r;
+      double s = 0.0;
+      if (has && !pv[r] && i != p) {
+        const double* xi = a.X + (size_t)i * n;
+        for (int j = gl; j < k; j += 16) s = fma(__ldcg(xi + j), xp[j], s);
+      }
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (has && gl == 0) {
+        double x;
+        if (i == p) {
+          x = dp * rsq;  // = sqrt(dp)
+          pv[r] = 1;
+          dl[r] = 0.0;
+        } else if (pv[r]) {
+          x = 0.0;
+        } else {
+          x = (a.B[(size_t)i * a.ldb + p] - s) * rsq;
+          dl[r] = dl[r] - x * x;
+        }
+        a.X[(size_t)i * n + k] = x;
+      }
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    a.info[2] = nonfinite ? 0 : k;
+    a.info[6] = nonfinite ? 1 : 0;
+    *a.K_out = nonfinite ? 0 : k;
+  }
+}
+
+// X (row-major, n x K) -> columns (column j contiguous, ld ldc), zero columns up to Kpad
+__global__ void wide_to_cols(const double* X, int n, const int* Kp, int Kmax, double* C, int ldc) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)Kmax * ldc) return;
+  const int j = (int)(e / ldc), i = (int)(e % ldc);
+  C[e] = (j < *Kp && i < n) ? X[(size_t)i * n + j] : 0.0;
+}
+
+__global__ void wide_set_int(int* p, int v) { *p = v; }
+
+// SVD mode: columns given (N of length dot, ld ldin) + identity accumulator rows
+__global__ void wide_load_svd(const double* in, int ldin, int N, int dot, int dpad, int Kmax, double* C,
+                              int ldc) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)Kmax * ldc) return;
+  const int j = (int)(e / ldc), i = (int)(e % ldc);
+  double v = 0.0;
+  if (j < N) v = i < dot ? in[(size_t)j * ldin + i] : (i - dpad == j ? 1.0 : 0.0);
+  C[e] = v;
+}
+
+// --------------------------------------------------- 2. block Jacobi sweeps --
+struct BjArgs {
+  double* C;  // columns, ld ldc
+  int ldc;
+  int L;      // rows per column (dot rows + accumulator rows)
+  int dot;    // rows entering the Gram
+  int nb;     // blocks (even), columns = nb * 16
+  double tol2, skip2;
+  int max_sweeps;
+  int* flag;  // [2] rotation flags per sweep parity
+  int* info;  // info[0] sweeps, info[1] converged
+};
+
+__global__ void __launch_bounds__(WT, 1) wide_bjacobi_kernel(const BjArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ __align__(16) double Ys[WCH * WLD];
+  __shared__ double Gs[WPC][WPC + 1];
+  __shared__ double Ws[WPC][WLD];
+  __shared__ int s_any;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int nb = a.nb, njobs = nb / 2;
+  int sweep = 0;
+  bool converged = false;
+  for (; sweep < a.max_sweeps; ++sweep) {
+    if (blockIdx.x == 0 && tid == 0) a.flag[(sweep + 1) & 1] = 0;
+    for (int r = 0; r < nb - 1; ++r) {
+      for (int job = blockIdx.x; job < njobs; job += gridDim.x) {
+        const int bp = job ? 1 + (job - 1 + r) % (nb - 1) : 0;
+        const int bq = 1 + (nb - 2 - job + r) % (nb - 1);
+        // column c of the job (0..31) -> global column
+        auto gcol = [&](int c) { return (c < WBS ? bp * WBS + c : bq * WBS + c - WBS); };
+        // ---- A. Gram of the 32 columns over the dot rows (DMMA; warp w: tile (w/4, w%4))
+        const int ti = warp >> 2, tj = warp & 3;
+        double acc[2] = {0.0, 0.0};
+        for (int r0 = 0; r0 < a.dot; r0 += WCH) {
+          for (int e = tid; e < WCH * WPC; e += WT) {
+            const int c = e / WCH, rr = e % WCH;
+            const int row = r0 + rr;
+            Ys[rr * WLD + c] = row < a.dot ? __ldcg(a.C + (size_t)gcol(c) * a.ldc + row) : 0.0;
+          }
+          __syncthreads();
+#pragma unroll 4
+          for (int kk = 0; kk < WCH / 4; ++kk) {
+            const double fa = Ys[(kk * 4 + t) * WLD + ti * 8 + g];
+            const double fb = Ys[(kk * 4 + t) * WLD + tj * 8 + g];
+            dmma(acc, fa, fb);
+          }
+          __syncthreads();
+        }
+        Gs[ti * 8 + g][tj * 8 + 2 * t] = acc[0];
+        Gs[ti * 8 + g][tj * 8 + 2 * t + 1] = acc[1];
+        for (int e = tid; e < WPC * WPC; e += WT) Ws[e / WPC][e % WPC] = (e / WPC == e % WPC) ? 1.0 : 0.0;
+        if (tid == 0) s_any = 0;
+        __syncthreads();
+        // ---- B. any pair above the rotation threshold?
+        {
+          int need = 0;
+          for (int e = tid; e < WPC * WPC; e += WT) {
+            const int i = e / WPC, j = e % WPC;
+            if (i < j) {
+              const double al = Gs[i][i], be = Gs[j][j], ga = Gs[i][j];
+              need |= (ga != 0.0 && ga * ga > a.tol2 * al * be && fmax(al, be) > a.skip2);
+            }
+          }
+          if (__syncthreads_or(need)) {
+            if (tid == 0) {
+              s_any = 1;
+              atomicOr(a.flag + (sweep & 1), 1);
+            }
+          }
+        }
+        __syncthreads();
+        if (!s_any) continue;  // uniform over the CTA
+        // ---- C. one sweep of two-sided Jacobi on Gs (circle ordering over 32 indices),
+        // W accumulates the rotations; warp w rotates pair w of the round
+        for (int rr = 0; rr < WPC - 1; ++rr) {
+          const int p = warp ? 1 + (warp - 1 + rr) % (WPC - 1) : 0;
+          const int q = 1 + (WPC - 2 - warp + rr) % (WPC - 1);
+          double c = 1.0, sn = 0.0;
+          const bool rot = wide_rot(Gs[p][p], Gs[q][q], Gs[p][q], a.tol2, a.skip2, c, sn);
+          __syncthreads();  // every warp has read its 2 x 2 block
+          if (rot) {  // rows p, q
+            const double gp = Gs[p][lane], gq = Gs[q][lane];
+            Gs[p][lane] = fma(c, gp, -sn * gq);
+            Gs[q][lane] = fma(sn, gp, c * gq);
+          }
+          __syncthreads();
+          if (rot) {  // columns p, q of G and W
+            const double gp = Gs[lane][p], gq = Gs[lane][q];
+            Gs[lane][p] = fma(c, gp, -sn * gq);
+            Gs[lane][q] = fma(sn, gp, c * gq);
+            const double wp = Ws[lane][p], wq = Ws[lane][q];
+            Ws[lane][p] = fma(c, wp, -sn * wq);
+            Ws[lane][q] = fma(sn, wp, c * wq);
+          }
+        }
+        __syncthreads();
+        // ---- D. Y <- Y W over all rows (DMMA; chunk 64 x 32 = 8 x 4 tiles, 2 per warp)
+        for (int r0 = 0; r0 < a.L; r0 += WCH) {
+          for (int e = tid; e < WCH * WPC; e += WT) {
+            const int c = e / WCH, rr = e % WCH;
+            const int row = r0 + rr;
+            Ys[rr * WLD + c] = row < a.L ? __ldcg(a.C + (size_t)gcol(c) * a.ldc + row) : 0.0;
+          }
+          __syncthreads();
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int tile = warp * 2 + h, bi = tile >> 2, bj = tile & 3;
+            double o[2] = {0.0, 0.0};
+#pragma unroll
+            for (int kk = 0; kk < WPC / 4; ++kk)
+              dmma(o, Ys[(bi * 8 + g) * WLD + kk * 4 + t], Ws[kk * 4 + t][bj * 8 + g]);
+            const int row = r0 + bi * 8 + g;
+            if (row < a.L) {
+              a.C[(size_t)gcol(bj * 8 + 2 * t) * a.ldc + row] = o[0];
+              a.C[(size_t)gcol(bj * 8 + 2 * t + 1) * a.ldc + row] = o[1];
+            }
+          }
+          __syncthreads();
+        }
+      }
+      grid.sync();
+    }
+    // end of the sweep: did any job rotate?
+    const int any = __ldcg(a.flag + (sweep & 1));
+    grid.sync();  // everyone has read the flag before the next sweep's reset of the other parity
+    if (!any) {
+      converged = true;
+      ++sweep;
+      break;
+    }
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    a.info[0] = sweep;
+    a.info[1] = converged ? 1 : 0;
+  }
+}
+
+// ------------------------------------------------------ 3. order and output --
+// norms over the dot rows, rank by descending norm (ties by index), output column rk:
+// dot rows normalised, then the accumulator rows (SVD); EIG slots [K, nout) zero.
+__global__ void wide_norms(const double* C, int ldc, int dot, int ncols, double* nrm) {
+  const int j = blockIdx.x;
+  if (j >= ncols) return;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < dot; i += blockDim.x) s = fma(C[(size_t)j * ldc + i], C[(size_t)j * ldc + i], s);
+  __shared__ double red[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+    nrm[j] = tot;
+  }
+}
+
+__global__ void wide_output(const double* C, int ldc, int L, int dot, int dpad, int ncols, const int* Kp,
+                            const double* nrm, int mode, int nout, double* out, int ldout, double* vals) {
+  const int j = blockIdx.x;  // source column
+  if (j >= ncols) return;
+  const int K = *Kp;
+  const double nj = nrm[j];
+  int rk = 0;
+  if (j < K) {
+    for (int i = 0; i < K; ++i) {
+      const double ni = nrm[i];
+      rk += (ni > nj) || (ni == nj && i < j);
+    }
+  } else {
+    rk = j;  // EIG: zero slots keep their position (past K)
+  }
+  if (rk >= nout) return;
+  const double nn = sqrt(nj);
+  const double inv = (j < K && nn > 0.0) ? 1.0 / nn : 0.0;
+  double* dst = out + (size_t)rk * ldout;
+  for (int i = threadIdx.x; i < L; i += blockDim.x) {
+    const double x = C[(size_t)j * ldc + i];
+    if (i < dot) dst[i] = x * inv;
+    else if (i >= dpad && j < K) dst[dot + (i - dpad)] = x;
+    else if (i >= dpad) dst[dot + (i - dpad)] = 0.0;
+  }
+  if (threadIdx.x == 0) vals[rk] = j < K ? (mode == 0 ? nj : nn) : 0.0;
+}
+
+// ------------------------------------------------------------ launchers ----
+static int wide_grid(int max_jobs_or_rows) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wide_bjacobi_kernel, WT, 0);
+  const int cap = std::max(1, per_sm) * dev_info().sms;
+  return std::max(1, std::min(cap, max_jobs_or_rows));
+}
+
+static size_t pad_even(size_t x) { return (x + 1) & ~size_t(1); }
+
+size_t jacobi_wide_workspace(int n, int L) {
+  const int kmax = ((n + WPC - 1) / WPC) * WPC;
+  const size_t ldc = pad_even(std::max(n, L));
+  return (size_t)n * n          // X row-major (EIG)
+         + (size_t)kmax * ldc   // columns
+         + (size_t)kmax         // norms
+         + 4 * 256 + 64;        // candidates, flags, K
+}
+
+static cudaError_t run_sweeps(double* C, int ldc, int L, int dot, int kmax, double tol, int max_sweeps,
+                              int* flag, int* info, cudaStream_t s) {
+  BjArgs b{};
+  b.C = C;
+  b.ldc = ldc;
+  b.L = L;
+  b.dot = dot;
+  b.nb = kmax / WBS;
+  b.tol2 = tol * tol;
+  b.skip2 = 0.0;  // (per-column floor below: zero columns never rotate, their dot products are 0)
+  b.max_sweeps = max_sweeps;
+  b.flag = flag;
+  b.info = info;
+  cudaError_t e = cudaMemsetAsync(flag, 0, 2 * sizeof(int), s);
+  if (e != cudaSuccess) return e;
+  const int grid = wide_grid(b.nb / 2);
+  void* args[] = {&b};
+  return cudaLaunchCooperativeKernel((void*)wide_bjacobi_kernel, grid, WT, args, 0, s);
+}
+
+cudaError_t launch_jacobi_eig_wide(const double* B, int ldb, int n, double tol, double trunc, int max_sweeps,
+                                   double* vecs, int ldv, double* vals, int* info, double* work,
+                                   cudaStream_t s) {
+  if (n < 1 || n > 2048) return cudaErrorInvalidValue;
+  const int kmax = ((n + WPC - 1) / WPC) * WPC;
+  const int ldc = (int)pad_even(n);
+  double* X = work;
+  double* C = X + (size_t)n * n;
+  double* nrm = C + (size_t)kmax * ldc;
+  double* cval = nrm + kmax;
+  int* ints = reinterpret_cast<int*>(cval + 2 * 256);
+  int* cidx = ints;         // [2][256]
+  int* flag = ints + 512;   // [2]
+  int* Kp = ints + 514;     // [1]
+  cudaError_t e = cudaMemsetAsync(info, 0, 8 * sizeof(int), s);
+  if (e != cudaSuccess) return e;
+  PcholArgs pa{};
+  pa.B = B;
+  pa.ldb = ldb;
+  pa.n = n;
+  pa.trunc = trunc;
+  pa.X = X;
+  pa.cval = cval;
+  pa.cidx = cidx;
+  pa.info = info;
+  pa.K_out = Kp;
+  int per_sm = 0;
+  const int rows_grid = std::min(256, dev_info().sms);
+  const size_t smem = ((size_t)n + (n + rows_grid - 1) / rows_grid * 2) * 8 + 64;
+  e = cudaFuncSetAttribute(wide_pchol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessorWithFlags(&per_sm, wide_pchol_kernel, WT, smem, 0);
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  void* pargs[] = {&pa};
+  e = cudaLaunchCooperativeKernel((void*)wide_pchol_kernel, rows_grid, WT, pargs, smem, s);
+  if (e != cudaSuccess) return e;
+  wide_to_cols<<<(unsigned)(((int64_t)kmax * ldc + 255) / 256), 256, 0, s>>>(X, n, Kp, kmax, C, ldc);
+  e = run_sweeps(C, ldc, n, n, kmax, tol, max_sweeps, flag, info, s);
+  if (e != cudaSuccess) return e;
+  wide_norms<<<kmax, 256, 0, s>>>(C, ldc, n, kmax, nrm);
+  wide_output<<<kmax, 256, 0, s>>>(C, ldc, n, n, n, kmax, Kp, nrm, 0, n, vecs, ldv, vals);
+  // eigenvector slots [kmax, n) (past the padded columns) are zero as well
+  if (kmax < n) {
+    for (int j = kmax; j < n; ++j) {
+      e = cudaMemsetAsync(vecs + (size_t)j * ldv, 0, (size_t)n * 8, s);
+      if (e != cudaSuccess) return e;
+    }
+    e = cudaMemsetAsync(vals + kmax, 0, (size_t)(n - kmax) * 8, s);
+  }
+  return e == cudaSuccess ? cudaGetLastError() : e;
+}
+
+cudaError_t launch_jacobi_svd_wide(const double* cols, int ldc_in, int N, int dot, double tol, int max_sweeps,
+                                   double* out, int ldout, double* vals, int* info, double* work,
+                                   cudaStream_t s) {
+  if (N < 1 || N > 2048 || dot < 1 || dot > 2048) return cudaErrorInvalidValue;
+  const int kmax = ((N + WPC - 1) / WPC) * WPC;
+  const int dpad = (int)pad_even(dot);
+  const int L = dpad + N;
+  const int ldc = (int)pad_even(L);
+  const int nx = std::max(N, dot);
+  double* C = work + (size_t)nx * nx;
+  double* nrm = C + (size_t)kmax * ldc;
+  double* cval = nrm + kmax;
+  int* ints = reinterpret_cast<int*>(cval + 2 * 256);
+  int* flag = ints + 512;
+  int* Kp = ints + 514;
+  cudaError_t e = cudaMemsetAsync(info, 0, 8 * sizeof(int), s);
+  if (e != cudaSuccess) return e;
+  wide_set_int<<<1, 1, 0, s>>>(Kp, N);
+  wide_load_svd<<<(unsigned)(((int64_t)kmax * ldc + 255) / 256), 256, 0, s>>>(cols, ldc_in, N, dot, dpad, kmax, C,
+                                                                             ldc);
+  e = run_sweeps(C, ldc, L, dot, kmax, tol, max_sweeps, flag, info, s);
+  if (e != cudaSuccess) return e;
+  wide_norms<<<kmax, 256, 0, s>>>(C, ldc, dot, kmax, nrm);
+  wide_output<<<kmax, 256, 0, s>>>(C, ldc, L, dot, dpad, kmax, Kp, nrm, 1, N, out, ldout, vals);
+  return cudaGetLastError();
+}
+
+}  // namespace tsk

@@ -72,4 +72,15 @@ cudaError_t launch_jacobi_svd(const double* cols, int ldc, int N, int ldot, doub
                               int max_sweeps, double* out, int ldout, double* vals, int* info,
                               cudaStream_t s);
 
+// ---- wide cores, 256 < n <= 2048 (jacobi_wide.cu): cooperative multi-CTA solvers ----
+// Same contracts as launch_jacobi_eig / launch_jacobi_svd, plus a device workspace of
+// jacobi_wide_workspace(n, L) doubles (n = order / max(N, dot), L = rows per column).
+size_t jacobi_wide_workspace(int n, int L);
+cudaError_t launch_jacobi_eig_wide(const double* B, int ldb, int n, double tol, double trunc, int max_sweeps,
+                                   double* vecs, int ldv, double* vals, int* info, double* work,
+                                   cudaStream_t s);
+cudaError_t launch_jacobi_svd_wide(const double* cols, int ldc, int N, int dot, double tol, int max_sweeps,
+                                   double* out, int ldout, double* vals, int* info, double* work,
+                                   cudaStream_t s);
+
 }  // namespace tsk

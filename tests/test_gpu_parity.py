@@ -109,10 +109,11 @@ def test_matmul_tn_kernel_vs_numpy(m, n, l):
     assert np.all(np.abs(z - ref) <= 1e-14 * m * (np.abs(x).T @ np.abs(y[:, :l])) + 1e-300)
 
 
-@pytest.mark.parametrize("n", [2, 9, 10, 55, 65, 72, 97, 100, 121, 128, 200, 256])
+@pytest.mark.parametrize("n", [2, 9, 10, 55, 65, 72, 97, 100, 121, 128, 200, 256, 257, 300, 777, 2000])
 def test_jacobi_eig_properties(n):
     """B V = V diag(lambda), V^T V = I, and lambda vs LAPACK on a well-conditioned Gram.
-    n in 65..128 runs the warp-block sweep ordering (with partial and zero-padded blocks)."""
+    n in 65..128 runs the warp-block sweep ordering (with partial and zero-padded blocks);
+    n > 256 the cooperative multi-CTA solver (left-looking pivoted Cholesky + block Jacobi)."""
     rng = np.random.default_rng(n)
     a = rng.standard_normal((3 * n, n))
     b = a.T @ a
