@@ -207,6 +207,7 @@ struct Pass {
 };
 
 inline int mrows_for(int k) { return (int)(gemm_nn_m_doubles(k, 1) / smem_ld(1)); }
+inline int64_t even(int64_t x) { return (x + 1) & ~int64_t(1); }
 
 // ---------------------------------------------------------------- core ----
 // Buffers of one Alg. 3/4 run on an (m_local x w) matrix.
@@ -514,6 +515,217 @@ CoreOut core(Ctx& c, Core& b, const double* X, int64_t ldx, int64_t m_local, int
   return out;
 }
 
+// ------------------------------------------------------------ wide core ----
+// Alg. 3/4 for 256 < w <= 2048 (the paper's n = 2000 workloads, Tables 3-5 / 19-21).  The
+// same steps as core(); what changes is the shape of the work:
+//   * Grams: block columns of 128 by the A^T Y kernel (gemm_tn with Y = the panel of the
+//     same matrix), lower block columns only, then mirrored;
+//   * products with more than 256 columns (Y~ = A V~, Q~ norms, U = Y~ M2): column panels
+//     of <= 256 through gemm_nn; Y~ lives in the workspace (m_local x K), so the final U may
+//     still alias A (A is not read after the A V~ pass);
+//   * the eigensolver / SVD of width > 256: the cooperative solvers of jacobi_wide.cu;
+//   * host decisions for k and r (the panels are sized by them), r' on the device.
+constexpr int kWideMax = 2048, kPanel = 256, kGramPanel = 128;
+
+struct WideCore {
+  int w = 0;
+  double *tnpart, *Yw, *B, *Bp, *lam, *nsq, *sig, *Mp, *Mfull, *G, *Z, *dz, *tsq, *T, *Rt, *sv, *Ps, *vj, *jw;
+  double* npart;
+  int *idx, *idx2, *info;
+  int64_t ldyw = 0;
+  void alloc(Arena& a, int64_t m, int ww) {
+    w = ww;
+    const int64_t mm = std::max<int64_t>(m, 1);
+    size_t tn = 0;
+    for (int j0 = 0; j0 < ww; j0 += kGramPanel)
+      tn = std::max(tn, plan_gemm_tn(mm, ww - j0, std::min(kGramPanel, ww - j0)).part_doubles);
+    tnpart = a.get<double>(tn);
+    ldyw = even(ww);
+    Yw = a.get<double>((size_t)mm * ldyw);
+    B = a.get<double>((size_t)ww * ww);
+    Bp = a.get<double>((size_t)ww * (ww + 1) / 2);
+    lam = a.get<double>(ww);
+    nsq = a.get<double>(ww);
+    sig = a.get<double>(ww);
+    Mp = a.get<double>(gemm_nn_m_doubles(ww, kPanel));
+    Mfull = a.get<double>((size_t)ww * ww);
+    G = a.get<double>((size_t)ww * ww);
+    Z = a.get<double>((size_t)ww * ww);
+    dz = a.get<double>(ww);
+    tsq = a.get<double>(ww);
+    T = a.get<double>(ww);
+    Rt = a.get<double>((size_t)ww * (3 * ww + 2));
+    sv = a.get<double>(ww);
+    Ps = a.get<double>((size_t)ww * ww);
+    vj = a.get<double>((size_t)ww * ww);
+    jw = a.get<double>(jacobi_wide_workspace(ww, 2 * ww + 2));
+    size_t nn = 0;
+    for (int q = 1; q <= kPanel; ++q) nn = std::max(nn, (size_t)gemm_nn_grid(mm, q) * gemm_nn_part_stride(q));
+    npart = a.get<double>(nn);
+    idx = a.get<int>(ww);
+    idx2 = a.get<int>(ww);
+    info = a.get<int>(8);
+  }
+};
+
+// G (w x w, ld ldg) = X^T X over the local rows: lower block columns of 128 by gemm_tn with
+// Y = X's own panel, reduced in a fixed order, mirrored; aggregated (packed) across ranks.
+void wide_gram(Ctx& c, Ctx& cd, WideCore& b, const double* X, int64_t ldx, int64_t m_local, int w, double* G,
+               int ldg, int pass_kind) {
+  cudaStream_t s = c.s;
+  {
+    Pass t(s, pass_kind, (double)m_local * w * (w + 1), 8.0 * m_local * w);
+    for (int j0 = 0; j0 < w; j0 += kGramPanel) {
+      const int l = std::min(kGramPanel, w - j0);
+      const TnPlan tp = plan_gemm_tn(std::max<int64_t>(m_local, 1), w - j0, l);
+      KL(launch_gemm_tn(tp, X + j0, ldx, m_local, w - j0, X + j0, ldx, l, b.tnpart, s));
+      KL(launch_reduce_parts_2d(b.tnpart, tp.splits, (int64_t)tp.colblocks * tp.cb * tp.ldz, w - j0, tp.ldz, l,
+                                G + (size_t)j0 * ldg + j0, ldg, false, s));
+    }
+    KS(symmetrize(G, w, ldg, s));
+  }
+  if (cd.dist()) {
+    KS(pack_lower(G, w, ldg, b.Bp, s));
+    allreduce(cd, b.Bp, (int64_t)w * (w + 1) / 2, "gram");
+    KS(unpack_sym(b.Bp, w, G, ldg, s));
+  }
+}
+
+// Y (m x c) = X (m x k) M with M given row-major (k x c, ld ldm): column panels of <= 256
+void wide_product(Ctx& c, WideCore& b, const double* X, int64_t ldx, int64_t m_local, int k, const double* M,
+                  int ldm, int cols, double* Y, int64_t ldy, double* nsq_out, int pass_kind) {
+  cudaStream_t s = c.s;
+  Pass t(s, pass_kind, 2.0 * m_local * k * cols, 8.0 * m_local * (k + cols));
+  for (int c0 = 0; c0 < cols; c0 += kPanel) {
+    const int cw = std::min(kPanel, cols - c0);
+    KS(rows_to_m(M + c0, ldm, k, cw, b.Mp, smem_ld(cw), mrows_for(k), s));
+    KL(launch_gemm_nn(X, ldx, m_local, k, b.Mp, cw, Y ? Y + c0 : nullptr, ldy, nsq_out ? b.npart : nullptr,
+                      nullptr, s));
+    if (nsq_out)
+      KL(launch_reduce_parts(b.npart, gemm_nn_grid(std::max<int64_t>(m_local, 1), cw), gemm_nn_part_stride(cw), cw,
+                             nsq_out + c0, s));
+  }
+}
+
+int wide_eig(Ctx& c, WideCore& b, double* Bm, int n, double* vals, double trunc, bool sync, const int** nf,
+             const char* what) {
+  step("eig:%s", what);
+  int* info = sync ? b.info : c.next_info();
+  {
+    Pass t(c.s, TSSVD_PASS_JACOBI, 0, 0);
+    if (n <= 256)
+      KL(launch_jacobi_eig(Bm, n, n, jacobi_tol(n), trunc, c.max_sweeps, Bm, n, vals, info, c.s));
+    else
+      KL(launch_jacobi_eig_wide(Bm, n, n, jacobi_tol(n), trunc, c.max_sweeps, Bm, n, vals, info, b.jw, c.s));
+  }
+  *nf = info + 6;
+  if (!sync) return n;
+  step("sync:k_%s", what);
+  int h[7];
+  read_ints(c, info, 7, h, n);
+  if (g_dry) return n;
+  if (g_stats.n_jacobi < 16) g_stats.jacobi_sweeps[g_stats.n_jacobi++] = h[0];
+  if (h[6]) fail(TSSVD_ENONFINITE, "non-finite entries in the input (Gram diagonal)");
+  if (!h[1]) fail(TSSVD_ENOCONV, "Jacobi eig (N=%d) not converged in %d sweeps", n, h[0]);
+  return h[2];
+}
+
+CoreOut core_wide(Ctx& c, WideCore& b, const double* X, int64_t ldx, int64_t m_local, int w, int passes,
+                  bool dist, double* U, int64_t ldu, double* sigma, double* V, int64_t ldv, double* Upack) {
+  cudaStream_t s = c.s;
+  Ctx cd = c;
+  if (!dist) cd.comm = nullptr;
+  step("core_wide:%s:%d:%d", dist ? "sharded" : "local", passes, w);
+  const double trunc = std::max(kEps, 0.01 * c.wp);  // reading R13, as in core()
+  // Step 1 (P:613 / P:646): B = A^* A
+  step("gram:X");
+  wide_gram(c, cd, b, X, ldx, m_local, w, b.B, w, TSSVD_PASS_GRAM_X);
+  // Step 2 (P:615 / P:648): B = V~ D V~^*  (k read back: it sizes the panels)
+  const int* nf = nullptr;
+  const int k = wide_eig(c, b, b.B, w, b.lam, trunc, true, &nf, "B");
+  CoreOut out;
+  if (k == 0) {
+    out.exact = true;
+    return out;
+  }
+  // Steps 3-4: Y~ = A V~ (k columns, into the workspace) and its column sums of squares
+  step("xv:%d", k);
+  // M = V~ (w x k row-major, ld k): eigenvector j is contiguous at B + j w
+  KS(cols_to_m(b.B, w, w, k, b.Mfull, k, w, s));
+  wide_product(c, b, X, ldx, m_local, w, b.Mfull, k, k, b.Yw, b.ldyw, b.nsq, TSSVD_PASS_XV);
+  ++g_stats.a_passes;
+  allreduce(cd, b.nsq, k, "norms");
+  // Step 5: discard (r, nc read back)
+  step("discard:1");
+  const int s1 = c.next_slot();
+  int* d1 = c.slot(s1);
+  KS(discard(b.nsq, k, c.wp, b.sig, b.idx, d1, nf, s));
+  int r = k, nc = k;
+  decide_now(c, s1, &r, &nc, k, "first discard");
+  if (r == 0) {
+    out.slot = s1;
+    out.exact = true;
+    return out;
+  }
+  double* Uo = Upack ? Upack : U;
+  if (passes == 1) {  // Step 6: U = Y~ Sigma^-1 (kept columns sorted, signs fixed)
+    step("alg3_out");
+    KS(fill(b.Mfull, (int64_t)nc * r, 0.0, s));
+    KS(alg3_out(b.sig, b.idx, d1, r, b.B, w, b.Mfull, r, sigma, V, ldv, s));
+    step("uout:%d", r);
+    wide_product(c, b, b.Yw, b.ldyw, m_local, nc, b.Mfull, r, r, Uo, Upack ? (r + 1) & ~1 : ldu, nullptr,
+                 TSSVD_PASS_UOUT);
+    out.bound = r;
+    out.slot = s1;
+    out.exact = true;
+    return out;
+  }
+  // Steps 6-7: Z = Sigma~^-1 (Y~^* Y~)_keep Sigma~^-1
+  step("gram:Y:%d", nc);
+  wide_gram(c, cd, b, b.Yw, b.ldyw, m_local, nc, b.G, nc, TSSVD_PASS_GRAM_Y);
+  const int rb = r;
+  step("build_z");
+  KS(build_z(b.G, nc, b.idx, b.sig, d1, rb, b.Z, s));
+  // Step 8: Z = W D W^*
+  const int* nfz = nullptr;
+  const int kz = wide_eig(c, b, b.Z, rb, b.dz, trunc, false, &nfz, "Z");
+  // Steps 9-10: T = column norms of Q~ = Y W (norms only)
+  step("qnorm:%d", kz);
+  KS(fill(b.Mfull, (int64_t)nc * kz, 0.0, s));
+  KS(build_m1(b.Z, rb, b.idx, b.sig, d1, rb, kz, b.Mfull, kz, s));
+  wide_product(c, b, b.Yw, b.ldyw, m_local, nc, b.Mfull, kz, kz, nullptr, 0, b.tsq, TSSVD_PASS_QNORM);
+  allreduce(cd, b.tsq, kz, "norms");
+  // Step 11: discard r' (on the device)
+  step("discard:2");
+  const int s2 = c.next_slot();
+  int* d2 = c.slot(s2);
+  KS(discard(b.tsq, kz, c.wp, b.T, b.idx2, d2, nfz, s));
+  const int rb2 = kz;
+  // Steps 12-14: SVD of K = T W_keep^T Sigma~ (r' x r)
+  step("svd:R");
+  KS(build_k(b.T, b.idx2, d2, rb2, b.Z, rb, d1, rb, b.sig, b.idx, b.Rt, s));
+  {
+    Pass t(s, TSSVD_PASS_JACOBI, 0, 0);
+    if (rb <= 256 && rb2 <= 256)
+      KL(launch_jacobi_svd(b.Rt, rb2, rb, rb2, jacobi_tol(rb2), c.max_sweeps, b.Rt + (size_t)rb2 * rb, rb2 + rb,
+                           b.sv, c.next_info(), s));
+    else
+      KL(launch_jacobi_svd_wide(b.Rt, rb2, rb, rb2, jacobi_tol(rb2), c.max_sweeps, b.Rt + (size_t)rb2 * rb,
+                                rb2 + rb, b.sv, c.next_info(), b.jw, s));
+  }
+  KS(wide_svd_out(b.Rt + (size_t)rb2 * rb, rb2 + rb, d2, rb2, d1, rb, b.sv, b.B, w, b.idx, sigma, V, ldv, b.Ps,
+                  b.vj, s));
+  // Step 15: U = Q P = Y~[:, :nc] M2
+  step("uout:%d", rb2);
+  KS(fill(b.Mfull, (int64_t)nc * rb2, 0.0, s));
+  KS(wide_build_m2(b.Z, rb, d1, rb, b.idx, b.sig, b.T, b.idx2, d2, rb2, b.Ps, b.Mfull, rb2, s));
+  wide_product(c, b, b.Yw, b.ldyw, m_local, nc, b.Mfull, rb2, rb2, Uo, Upack ? (rb2 + 1) & ~1 : ldu, nullptr,
+               TSSVD_PASS_UOUT);
+  out.bound = rb2;
+  out.slot = s2;
+  return out;
+}
+
 // kept rank of a finished core
 int64_t core_rank(const CoreOut& o, const Finish& f) {
   if (o.slot < 0) return 0;
@@ -559,6 +771,7 @@ bool devmode_for(int w) {
 
 struct TsPlan {
   Core core;
+  WideCore wide;
   int* ctl;
   double* a_stage;  // host_io: device copy of A (also holds Y~)
   double* u_pack;   // host_io: U packed (ld (r+1)&~1) for one contiguous D2H copy
@@ -566,11 +779,10 @@ struct TsPlan {
   double* v_stage;
 };
 
-inline int64_t even(int64_t x) { return (x + 1) & ~int64_t(1); }
-
 size_t plan_tssvd(Arena& a, TsPlan& p, int64_t m_local, int n, const tssvd_opts* o) {
   p.ctl = a.get<int>(kCtlInts);
-  p.core.alloc(a, m_local, n);
+  if (n <= 256) p.core.alloc(a, m_local, n);
+  else p.wide.alloc(a, m_local, n);  // 256 < n <= 2048: m_local x n of workspace for Y~
   if (o && o->host_io) {
     p.a_stage = a.get<double>((size_t)std::max<int64_t>(m_local, 1) * even(n));
     p.u_pack = a.get<double>((size_t)std::max<int64_t>(m_local, 1) * even(n));
@@ -583,7 +795,7 @@ size_t plan_tssvd(Arena& a, TsPlan& p, int64_t m_local, int n, const tssvd_opts*
 // host_io: A is staged with an even leading dimension, so any lda >= n is accepted
 void validate_tall(int64_t m_local, int64_t n, int64_t lda, bool hio) {
   if (m_local < 0) fail(TSSVD_EINVAL, "m_local < 0");
-  if (n < 1 || n > 256) fail(TSSVD_EINVAL, "n = %lld must be in [1, 256]", (long long)n);
+  if (n < 1 || n > kWideMax) fail(TSSVD_EINVAL, "n = %lld must be in [1, %d]", (long long)n, kWideMax);
   if (lda < n || (!hio && (lda & 1)))
     fail(TSSVD_EINVAL, "lda = %lld must be even and >= n (16-byte TMA row strides)", (long long)lda);
 }
@@ -647,8 +859,10 @@ void tssvd_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, cons
     ldvd = n;
   }
   const bool packed = hio && ldu == 0;
-  const CoreOut o = core(c, p.core, X, ldx, m_local, (int)n, opts->orthonormalizations, true, Ud, ldud, sigd,
-                         Vd, ldvd, devmode_for((int)n), packed ? p.u_pack : nullptr);
+  const CoreOut o = n <= 256 ? core(c, p.core, X, ldx, m_local, (int)n, opts->orthonormalizations, true, Ud, ldud,
+                                    sigd, Vd, ldvd, devmode_for((int)n), packed ? p.u_pack : nullptr)
+                               : core_wide(c, p.wide, X, ldx, m_local, (int)n, opts->orthonormalizations, true, Ud,
+                                           ldud, sigd, Vd, ldvd, packed ? p.u_pack : nullptr);
   Finish f;
   finish(c, f);
   if (c.dist() && !g_dry && f.m < n)

@@ -40,5 +40,13 @@ void canon_lowrank(double* VA, int64_t ldva, int n, double* Ut, int ldut, int r3
                    cudaStream_t s);
 void copy2d(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int cols,
             cudaStream_t s);
+// wide core (wide_core.cu): Gram packing, V = V~_keep J with signs, M2 = S W T^-1 P
+void pack_lower(const double* B, int w, int ldb, double* packed, cudaStream_t s);
+void wide_svd_out(const double* cols, int ldc, const int* rr2, int rb2, const int* rr, int rb,
+                  const double* vals, const double* Vt, int w, const int* idx, double* sigma, double* V,
+                  int64_t ldv, double* Ps, double* vj_tmp, cudaStream_t s);
+void wide_build_m2(const double* W, int ldw, const int* rr, int rb, const int* idx, const double* sig,
+                   const double* T, const int* idx2, const int* rr2, int rb2, const double* Ps, double* M2, int ldm,
+                   cudaStream_t s);
 void fill(double* p, int64_t n, double v, cudaStream_t s);
 }  // namespace tsk

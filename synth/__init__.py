@@ -18,6 +18,8 @@ from .matrices import (  # noqa: F401
     dct_columns,
     paper_test_matrix,
     paper_lowrank_test_matrix,
+    devils_staircase,
+    paper_staircase_matrix,
     omega,
     power_start,
     config_inputs,

@@ -174,6 +174,28 @@ def paper_lowrank_test_matrix(m: int, n: int, l: int) -> tuple[np.ndarray, np.nd
     return a, s
 
 
+def devils_staircase(k: int) -> np.ndarray:
+    """Singular values of Appendix 'devil', restating its Scala recipe:
+    for j = 0..k-1, x = round(j * 8^6 / k) in single precision, the octal digits 1-7 of x
+    become binary 1s (octal 0 stays 0), read as a binary number, / 2^6 / (1 - 2^-6); sorted
+    descending.  Values are multiples of 1/63 in [0, 1], with many repeats."""
+    out = np.empty(k)
+    scale = np.float32(8.0 ** 6)
+    for j in range(k):
+        x = int(np.floor(np.float32(np.float32(j) * scale / np.float32(k)) + np.float32(0.5)))  # Math.round(float)
+        bits = "".join("0" if ch == "0" else "1" for ch in format(x, "o"))
+        out[j] = int(bits, 2) / 2.0 ** 6 / (1.0 - 2.0 ** -6)
+    return np.sort(out)[::-1].copy()
+
+
+def paper_staircase_matrix(m: int, n: int) -> tuple[np.ndarray, np.ndarray]:
+    """Eq. originalmat with the Devil's-staircase spectrum (k = n):
+    A = U Sigma V^*, U and V the DCT factors of Eq. originalmat; returns (A, sigma)."""
+    s = devils_staircase(n)
+    a = (dct_columns(m, n) * s[None, :]) @ dct_columns(n, n).T
+    return a, s
+
+
 def omega(n: int, l: int, seed: int) -> np.ndarray:
     """Alg. 5 step 1: n x l i.i.d. centred Gaussian start block, shared by both paths."""
     return normal_block(seed, STREAM_OMEGA, 0, n, l)

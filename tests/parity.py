@@ -69,3 +69,30 @@ def assert_lowrank_parity(gpu, ref, a, x0, *, uv_const: float = 1e3, ortho_tol: 
     out["spectral_error_gpu"], out["spectral_error_ref"] = eg, er
     assert abs(eg - er) <= 0.01 * er, out
     return out
+
+
+def assert_grouped_parity(gpu, ref, *, sigma_tol: float = 1e-10, ortho_tol: float = 1e-13, gap: float = 1e-8):
+    """Repeated singular values (the Devil's staircase, reading Q4): singular vectors are unique
+    only up to a rotation inside each group of equal sigma, so compare the SUBSPACES: for every
+    group (consecutive sigma_j within gap * sigma_1), the principal angles between the GPU's and the
+    oracle's column spaces (U and V alike) must be ~0 (sines <= 1e-9), besides sigma and
+    orthonormality as in assert_tssvd_parity."""
+    ug, sg, vg = gpu
+    ur, sr, vr = ref
+    assert sg.size == sr.size, f"kept rank differs: gpu {sg.size} vs oracle {sr.size}"
+    s1 = sr[0]
+    assert np.max(np.abs(sg - sr)) <= sigma_tol * s1
+    out = dict(ortho_u=oracle.ortho_error(ug), ortho_v=oracle.ortho_error(vg))
+    assert out["ortho_u"] <= ortho_tol and out["ortho_v"] <= ortho_tol, out
+    j, worst = 0, 0.0
+    while j < sr.size:
+        e = j + 1
+        while e < sr.size and abs(sr[e] - sr[j]) <= gap * s1:
+            e += 1
+        for a, b in ((ug, ur), (vg, vr)):
+            cosines = np.linalg.svd(a[:, j:e].T @ b[:, j:e], compute_uv=False)
+            worst = max(worst, float(np.sqrt(max(0.0, 1.0 - np.min(cosines) ** 2))))
+        j = e
+    out["max_subspace_sine"] = worst
+    assert worst <= 1e-9, out
+    return out

@@ -5,7 +5,7 @@ import pytest
 
 import oracle
 import synth
-from parity import assert_lowrank_parity, assert_tssvd_parity
+from parity import assert_grouped_parity, assert_lowrank_parity, assert_tssvd_parity
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -121,9 +121,12 @@ def test_jacobi_eig_properties(n):
     lam, v = lam.cpu().numpy(), v.cpu().numpy()
     assert np.all(np.diff(lam) <= 0)
     assert np.max(np.abs(v.T @ v - np.eye(n))) <= 1e-13
-    assert np.max(np.abs(b @ v - v * lam)) <= 1e-13 * lam[0]
+    # backward-error scale of a symmetric eigensolver: ~ n eps ||B|| (LAPACK's own error at
+    # n = 777 is ~1.7e-13 lambda_1), floored at the small cores' 1e-13
+    tol = max(1e-13, 2 * n * np.finfo(float).eps)
+    assert np.max(np.abs(b @ v - v * lam)) <= tol * lam[0]
     d, _ = oracle.sym_eig(b)
-    assert np.max(np.abs(lam - d)) <= 1e-13 * d[0]
+    assert np.max(np.abs(lam - d)) <= tol * d[0]
     assert sweeps < 30
 
 
@@ -585,3 +588,60 @@ def test_lowrank_c5_full_size_properties():
     err = torch.linalg.norm(A @ x - U @ (S * (V.T @ x))).item()
     sk1 = math.exp(-k / 15.0)
     assert abs(err - sk1) <= 0.01 * sk1 + noise
+
+
+# ------------------------------------------- wide cores (NEXT-1: n = 2000) --
+@pytest.mark.parametrize("m,n,passes,decades", [(3_000, 257, 2, 8), (5_000, 400, 1, 6), (5_000, 400, 2, 10),
+                                               (4_001, 1_000, 2, 8), (2_600, 2_048, 2, 6)])
+def test_tssvd_wide_vs_oracle(m, n, passes, decades):
+    """256 < n <= 2048: Gram block columns by the A^T Y kernel, the cooperative eigensolver /
+    SVD (left-looking pivoted Cholesky + block Jacobi), column-panel products; the parity
+    contract as for the narrow cores (decades = 10: the discard acts, r < n)."""
+    rng = np.random.default_rng(m + n)
+    sig = 10.0 ** (-decades * np.arange(n) / (n - 1))
+    u, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    v, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    a = (u * sig) @ v.T
+    gpu = run_tssvd(a, 1e-11, passes)
+    ref = oracle.tssvd(a, 1e-11, passes)
+    print(n, ref[1].size, assert_tssvd_parity(gpu, ref, passes=passes))
+
+
+def test_tssvd_paper_table5_gpu():
+    """PAPER.md:973 (Table 5, m = 1e4, n = 2000, Eq. originalmat + testS, DCT factors) on the GPU
+    path: Algorithm 4 at the reading-Q1 wp = 1e-12 against the oracle (r = 600) and against the
+    printed residual 9.64e-07 (the same 5% as the oracle pin) and orthonormality (10x printed)."""
+    import json
+    import os
+
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_values.json")))["alg4_m1e4_n2000"]
+    a, sig = synth.paper_test_matrix(g["m"], g["n"])
+    gpu = run_tssvd(a, 1e-12, 2)
+    ref = oracle.tssvd(a, 1e-12, 2)
+    info = assert_tssvd_parity(gpu, ref, passes=2)
+    err = oracle.spectral_error(a, *gpu, synth.power_start(g["n"], 7))
+    print(gpu[1].size, err, info)
+    assert err == pytest.approx(g["spectral_error"], rel=0.05)
+    assert info["ortho_u_gpu"] <= 10 * g["max_UtU_minus_I"] and info["ortho_v_gpu"] <= 10 * g["max_VtV_minus_I"]
+
+
+@pytest.mark.parametrize("passes,key", [(1, "staircase_alg3_m1e4_n2000"), (2, "staircase_alg4_m1e4_n2000")])
+def test_tssvd_paper_staircase_table21_gpu(passes, key):
+    """PAPER.md:1457-1458 (Table 21: the Devil's staircase, 36 distinct singular values, sigma = 1
+    with multiplicity 938, m = 1e4, n = 2000) on the GPU path: subspace parity with the oracle per
+    group of equal sigma (reading Q4), sigma against the constructed values, the printed residual
+    and orthonormality orders of magnitude."""
+    import json
+    import os
+
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_values.json")))[key]
+    a, sig = synth.paper_staircase_matrix(g["m"], g["n"])
+    gpu = run_tssvd(a, 1e-11, passes)
+    ref = oracle.tssvd(a, 1e-11, passes)
+    info = assert_grouped_parity(gpu, ref, ortho_tol=10 * g["max_UtU_minus_I"])
+    err = oracle.spectral_error(a, *gpu, synth.power_start(g["n"], 7))
+    print(passes, gpu[1].size, err, info)
+    assert gpu[1].size == g["n"] - 1
+    assert np.max(np.abs(gpu[1] - sig[: gpu[1].size])) <= 1e-12
+    assert g["spectral_error"] / 10 <= err <= 10 * g["spectral_error"]
+    assert info["ortho_v"] <= 10 * g["max_VtV_minus_I"]

@@ -317,3 +317,33 @@ def test_paper_table5_alg4():
     assert err == pytest.approx(g["spectral_error"], rel=0.05)
     assert oracle.ortho_error(u) <= 10 * g["max_UtU_minus_I"]
     assert oracle.ortho_error(v) <= 10 * g["max_VtV_minus_I"]
+
+
+def test_devils_staircase_recipe():
+    """PAPER.md:1351-1368 (the Scala recipe): every value is a multiple of 1/63 in [0, 1], the
+    binary image of the octal digits (1-7 -> 1) of round(j 8^6 / k); j = 0 is the only zero for
+    k = 2000; small k by hand: k = 8 -> round(j 8^5) octal j00000 -> binary j>0 ? 100000 : 0."""
+    g = PAPER["staircase_values"]
+    s = synth.devils_staircase(2000)
+    b = s * g["denominator"]
+    assert np.allclose(b, np.round(b), atol=1e-12) and s.max() == g["max"] and s.min() == 0.0
+    assert int(np.sum(s == 0.0)) == g["zeros_for_k_2000"]
+    assert np.all(np.diff(s) <= 0)
+    k8 = synth.devils_staircase(8)
+    assert np.allclose(k8, [32 / 63] * 7 + [0.0])
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("passes,key", [(1, "staircase_alg3_m1e4_n2000"), (2, "staircase_alg4_m1e4_n2000")])
+def test_paper_table21_staircase(passes, key):
+    """PAPER.md:1457-1458 (Table 21, Devil's staircase, m = 1e4, n = 2000): residual ~1e-14 and
+    orthonormality at the printed orders of magnitude; the kept rank drops only the one zero."""
+    g = PAPER[key]
+    a, sig = synth.paper_staircase_matrix(g["m"], g["n"])
+    u, s, v = oracle.tssvd(a, 1e-11, passes)
+    err = oracle.spectral_error(a, u, s, v, synth.power_start(g["n"], 7))
+    assert s.size == g["n"] - 1
+    assert g["spectral_error"] / 10 <= err <= 10 * g["spectral_error"]
+    assert oracle.ortho_error(u) <= 10 * g["max_UtU_minus_I"]
+    assert oracle.ortho_error(v) <= 10 * g["max_VtV_minus_I"]
+    assert np.max(np.abs(s - sig[: s.size])) <= 1e-12
