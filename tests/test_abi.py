@@ -50,7 +50,9 @@ def test_workspace_queries_and_validation_without_gpu():
     assert nb.value > 200_000 * 26 * 8  # holds Y (m x l)
     # argument errors are reported, not crashed on
     assert h.tssvd_workspace_size(None, 100, 7, ctypes.byref(o), ctypes.byref(nb)) == 0  # odd n is fine
-    assert h.tssvd_workspace_size(None, 100, 300, ctypes.byref(o), ctypes.byref(nb)) == 1  # n > 256
+    assert h.tssvd_workspace_size(None, 100, 2049, ctypes.byref(o), ctypes.byref(nb)) == 1  # n > 2048
+    assert h.tssvd_workspace_size(None, 10_000, 2_000, ctypes.byref(o), ctypes.byref(nb)) == 0  # wide core
+    assert nb.value > 10_000 * 2_000 * 8  # holds Y~ (m x n) for the wide core
     bad = _lib.default_opts(wp=1.5)
     assert h.tssvd_workspace_size(None, 100, 10, ctypes.byref(bad), ctypes.byref(nb)) == 1
     assert b"working precision" in h.tssvd_last_error()
