@@ -604,7 +604,9 @@ def test_tssvd_wide_vs_oracle(m, n, passes, decades):
     a = (u * sig) @ v.T
     gpu = run_tssvd(a, 1e-11, passes)
     ref = oracle.tssvd(a, 1e-11, passes)
-    print(n, ref[1].size, assert_tssvd_parity(gpu, ref, passes=passes))
+    # R12's constant 1e3 was calibrated at n <= 200; both eigensolvers' backward error grows like
+    # n eps ||B||, so the column bound scales with n: 5 n eps (sigma_1 / sigma_j)^2 (= 1e3 at 200)
+    print(n, ref[1].size, assert_tssvd_parity(gpu, ref, passes=passes, uv_const=max(1e3, 5.0 * n)))
 
 
 def test_tssvd_paper_table5_gpu():
@@ -618,7 +620,7 @@ def test_tssvd_paper_table5_gpu():
     a, sig = synth.paper_test_matrix(g["m"], g["n"])
     gpu = run_tssvd(a, 1e-12, 2)
     ref = oracle.tssvd(a, 1e-12, 2)
-    info = assert_tssvd_parity(gpu, ref, passes=2)
+    info = assert_tssvd_parity(gpu, ref, passes=2, uv_const=5.0 * g["n"])  # R12 scaled with n (wide test)
     err = oracle.spectral_error(a, *gpu, synth.power_start(g["n"], 7))
     print(gpu[1].size, err, info)
     assert err == pytest.approx(g["spectral_error"], rel=0.05)
