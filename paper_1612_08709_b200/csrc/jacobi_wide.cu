@@ -317,6 +317,20 @@ __global__ void __launch_bounds__(WT, 1) wide_bjacobi_kernel(const BjArgs a) {
           }
         }
         __syncthreads();
+        // W's columns back to unit norm: each rotation's c^2 + s^2 is 1 only to a few ulp, and
+        // over ~(blocks x sweeps) applications per column that norm drift (not the mutual
+        // orthogonality, which drifts at second order) made Y Y^T wander from B by ~1e-13
+        // relative on the paper's n = 2000 staircase (measured); one normalisation per job
+        // keeps every applied W orthogonal to rounding.
+        {
+          double s0 = 0.0, s1 = 0.0;
+          for (int i = lane; i < WPC; i += 32) s0 = fma(Ws[i][2 * warp], Ws[i][2 * warp], s0), s1 = fma(Ws[i][2 * warp + 1], Ws[i][2 * warp + 1], s1);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) s0 += __shfl_xor_sync(0xffffffffu, s0, o), s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+          const double i0 = rsqrt_nr_w(s0), i1 = rsqrt_nr_w(s1);
+          for (int i = lane; i < WPC; i += 32) Ws[i][2 * warp] *= i0, Ws[i][2 * warp + 1] *= i1;
+        }
+        __syncthreads();
         // ---- D. Y <- Y W over all rows (DMMA; chunk 64 x 32 = 8 x 4 tiles, 2 per warp)
         for (int r0 = 0; r0 < a.L; r0 += WCH) {
           for (int e = tid; e < WCH * WPC; e += WT) {

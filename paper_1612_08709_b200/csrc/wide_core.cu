@@ -90,10 +90,20 @@ __global__ void __launch_bounds__(256) k_wide_svd_sign(const double* VJ, int ldv
       if (sb[q] > b || (sb[q] == b && si[q] < i0)) b = sb[q], i0 = si[q], g = ss[q];
     ssg = g;
   }
+  // the column's norm (V~_keep J has unit columns in exact arithmetic; the accumulated
+  // rotations drift in norm at the rounding level): fixed-order block sum
+  double nn = 0.0;
+  for (int i = tid; i < w; i += blockDim.x) nn = fma(VJ[(size_t)i * ldvj + a], VJ[(size_t)i * ldvj + a], nn);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nn += __shfl_xor_sync(0xffffffffu, nn, o);
+  __shared__ double snn[8];
+  if (lane == 0) snn[warp] = nn;
   __syncthreads();
-  const double s = ssg;
+  double tot = 0.0;
+  for (int q = 0; q < (int)(blockDim.x >> 5); ++q) tot += snn[q];
+  const double s = ssg / sqrt(tot);
   for (int i = tid; i < w; i += blockDim.x) V[(size_t)i * ldv + a] = s * VJ[(size_t)i * ldvj + a];
-  for (int c = tid; c < rb2; c += blockDim.x) Ps[(size_t)a * rb2 + c] = c < r2 ? s * cols[(size_t)a * ldc + c] : 0.0;
+  for (int c = tid; c < rb2; c += blockDim.x) Ps[(size_t)a * rb2 + c] = c < r2 ? ssg * cols[(size_t)a * ldc + c] : 0.0;
   if (tid == 0) sigma[a] = vals[a];
 }
 

@@ -25,13 +25,26 @@ for name, (a, sig), wp in [("staircase", synth.paper_staircase_matrix(10_000, 2_
               "dsig", np.max(np.abs(sg - sr)) if sg.size == sr.size else None, flush=True)
         if sg.size != sr.size or name != "staircase":
             continue
+        vt = synth.dct_columns(2_000, 2_000)  # exact right singular vectors (Eq. originalmat)
+        resid_g = np.max(np.abs(a @ vg - ug * sg)) if passes else 0
+        resid_r = np.max(np.abs(a @ vr - ur * sr))
+        print("  max|A V - U S|: gpu", resid_g, "oracle", resid_r, flush=True)
+        j, wg, wr = 0, 0.0, 0.0
+        while j < sr.size:
+            e = j + 1
+            while e < sr.size and abs(sr[e] - sr[j]) <= 1e-8:
+                e += 1
+            wg = max(wg, np.linalg.norm(vg[:, j:e] - vt[:, j:e] @ (vt[:, j:e].T @ vg[:, j:e]), 2))
+            wr = max(wr, np.linalg.norm(vr[:, j:e] - vt[:, j:e] @ (vt[:, j:e].T @ vr[:, j:e]), 2))
+            j = e
+        print("  max sine to the TRUE right subspaces: gpu", wg, "oracle", wr, flush=True)
         j = 0
         while j < sr.size:
             e = j + 1
             while e < sr.size and abs(sr[e] - sr[j]) <= 1e-8:
                 e += 1
-            su = np.sqrt(max(0, 1 - np.min(np.linalg.svd(ug[:, j:e].T @ ur[:, j:e], compute_uv=False)) ** 2))
-            sv = np.sqrt(max(0, 1 - np.min(np.linalg.svd(vg[:, j:e].T @ vr[:, j:e], compute_uv=False)) ** 2))
+            su = np.linalg.norm(ug[:, j:e] - ur[:, j:e] @ (ur[:, j:e].T @ ug[:, j:e]), 2)
+            sv = np.linalg.norm(vg[:, j:e] - vr[:, j:e] @ (vr[:, j:e].T @ vg[:, j:e]), 2)
             if max(su, sv) > 1e-10:
                 print(f"  group [{j},{e}) sigma {sr[j]:.6f} sine U {su:.2e} V {sv:.2e}", flush=True)
             j = e
