@@ -447,7 +447,9 @@ static cudaError_t run_sweeps(double* C, int ldc, int L, int dot, int kmax, doub
   b.L = L;
   b.dot = dot;
   b.nb = kmax / WBS;
-  b.tol2 = tol * tol;
+  // TSSVD_WIDE_TOL scales the rotation threshold (experiments)
+  static const double tscale = getenv("TSSVD_WIDE_TOL") ? atof(getenv("TSSVD_WIDE_TOL")) : 1.0;
+  b.tol2 = tol * tol * tscale * tscale;
   b.skip2 = 0.0;  // (per-column floor below: zero columns never rotate, their dot products are 0)
   b.max_sweeps = max_sweeps;
   b.flag = flag;
