@@ -36,7 +36,8 @@ namespace tsk {
 static constexpr int WT = 512;   // threads per CTA
 static constexpr int WBS = 16;   // columns per block
 static constexpr int WPC = 32;   // columns per job (a block pair)
-static constexpr int WCH = 64;   // rows per streamed chunk
+static constexpr int WCH = 128;  // rows per streamed chunk (dynamic shared memory)
+static constexpr int WPER = WCH * 32 / 512;  // chunk elements per thread
 static constexpr int WLD = 36;   // smem row stride of a chunk (= 4 mod 8: conflict-free fragments)
 
 __device__ __forceinline__ double rsqrt_nr_w(double x) {
@@ -235,7 +236,7 @@ struct BjArgs {
 
 __global__ void __launch_bounds__(WT, 1) wide_bjacobi_kernel(const BjArgs a) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ __align__(16) double Ys[WCH * WLD];
+  extern __shared__ __align__(16) double Ys[];  // [WCH * WLD]
   __shared__ double Gs[WPC][WPC + 1];
   __shared__ double Ws[WPC][WLD];
   __shared__ int s_any;
@@ -251,16 +252,31 @@ __global__ void __launch_bounds__(WT, 1) wide_bjacobi_kernel(const BjArgs a) {
         const int bq = 1 + (nb - 2 - job + r) % (nb - 1);
         // column c of the job (0..31) -> global column
         auto gcol = [&](int c) { return (c < WBS ? bp * WBS + c : bq * WBS + c - WBS); };
+        // chunk loader: element q of thread tid -> (column c, chunk row rr); the next chunk is
+        // loaded into registers while the current one is consumed (one L2 round trip in flight)
+        auto load = [&](int r0, int lim, double (&v)[WPER]) {
+#pragma unroll
+          for (int q = 0; q < WPER; ++q) {
+            const int e = tid + q * WT, c = e / WCH, rr = e % WCH, row = r0 + rr;
+            v[q] = row < lim ? __ldcg(a.C + (size_t)gcol(c) * a.ldc + row) : 0.0;
+          }
+        };
+        auto stage = [&](const double (&v)[WPER]) {
+#pragma unroll
+          for (int q = 0; q < WPER; ++q) {
+            const int e = tid + q * WT;
+            Ys[(e % WCH) * WLD + e / WCH] = v[q];
+          }
+        };
         // ---- A. Gram of the 32 columns over the dot rows (DMMA; warp w: tile (w/4, w%4))
         const int ti = warp >> 2, tj = warp & 3;
         double acc[2] = {0.0, 0.0};
+        double cur[WPER], nxt[WPER];
+        load(0, a.dot, cur);
         for (int r0 = 0; r0 < a.dot; r0 += WCH) {
-          for (int e = tid; e < WCH * WPC; e += WT) {
-            const int c = e / WCH, rr = e % WCH;
-            const int row = r0 + rr;
-            Ys[rr * WLD + c] = row < a.dot ? __ldcg(a.C + (size_t)gcol(c) * a.ldc + row) : 0.0;
-          }
+          stage(cur);
           __syncthreads();
+          if (r0 + WCH < a.dot) load(r0 + WCH, a.dot, nxt);
 #pragma unroll 4
           for (int kk = 0; kk < WCH / 4; ++kk) {
             const double fa = Ys[(kk * 4 + t) * WLD + ti * 8 + g];
@@ -268,6 +284,8 @@ __global__ void __launch_bounds__(WT, 1) wide_bjacobi_kernel(const BjArgs a) {
             dmma(acc, fa, fb);
           }
           __syncthreads();
+#pragma unroll
+          for (int q = 0; q < WPER; ++q) cur[q] = nxt[q];
         }
         Gs[ti * 8 + g][tj * 8 + 2 * t] = acc[0];
         Gs[ti * 8 + g][tj * 8 + 2 * t + 1] = acc[1];
@@ -315,8 +333,8 @@ __global__ void __launch_bounds__(WT, 1) wide_bjacobi_kernel(const BjArgs a) {
             Ws[lane][p] = fma(c, wp, -sn * wq);
             Ws[lane][q] = fma(sn, wp, c * wq);
           }
+          __syncthreads();  // the next round reads 2 x 2 blocks this column phase wrote
         }
-        __syncthreads();
         // W's columns back to unit norm: each rotation's c^2 + s^2 is 1 only to a few ulp, and
         // over ~(blocks x sweeps) applications per column that norm drift (not the mutual
         // orthogonality, which drifts at second order) made Y Y^T wander from B by ~1e-13
@@ -331,17 +349,15 @@ __global__ void __launch_bounds__(WT, 1) wide_bjacobi_kernel(const BjArgs a) {
           for (int i = lane; i < WPC; i += 32) Ws[i][2 * warp] *= i0, Ws[i][2 * warp + 1] *= i1;
         }
         __syncthreads();
-        // ---- D. Y <- Y W over all rows (DMMA; chunk 64 x 32 = 8 x 4 tiles, 2 per warp)
+        // ---- D. Y <- Y W over all rows (DMMA; chunk 128 x 32 = 16 x 4 tiles, 4 per warp)
+        load(0, a.L, cur);
         for (int r0 = 0; r0 < a.L; r0 += WCH) {
-          for (int e = tid; e < WCH * WPC; e += WT) {
-            const int c = e / WCH, rr = e % WCH;
-            const int row = r0 + rr;
-            Ys[rr * WLD + c] = row < a.L ? __ldcg(a.C + (size_t)gcol(c) * a.ldc + row) : 0.0;
-          }
+          stage(cur);
           __syncthreads();
+          if (r0 + WCH < a.L) load(r0 + WCH, a.L, nxt);
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int tile = warp * 2 + h, bi = tile >> 2, bj = tile & 3;
+          for (int h = 0; h < WCH / 32; ++h) {
+            const int tile = warp * (WCH / 32) + h, bi = tile >> 2, bj = tile & 3;
             double o[2] = {0.0, 0.0};
 #pragma unroll
             for (int kk = 0; kk < WPC / 4; ++kk)
@@ -353,6 +369,8 @@ __global__ void __launch_bounds__(WT, 1) wide_bjacobi_kernel(const BjArgs a) {
             }
           }
           __syncthreads();
+#pragma unroll
+          for (int q = 0; q < WPER; ++q) cur[q] = nxt[q];
         }
       }
       grid.sync();
@@ -421,9 +439,9 @@ __global__ void wide_output(const double* C, int ldc, int L, int dot, int dpad, 
 }
 
 // ------------------------------------------------------------ launchers ----
-static int wide_grid(int max_jobs_or_rows) {
+static int wide_grid(int max_jobs_or_rows, size_t smem) {
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wide_bjacobi_kernel, WT, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wide_bjacobi_kernel, WT, smem);
   const int cap = std::max(1, per_sm) * dev_info().sms;
   return std::max(1, std::min(cap, max_jobs_or_rows));
 }
@@ -459,9 +477,12 @@ static cudaError_t run_sweeps(double* C, int ldc, int L, int dot, int kmax, doub
   b.info = info;
   cudaError_t e = cudaMemsetAsync(flag, 0, 2 * sizeof(int), s);
   if (e != cudaSuccess) return e;
-  const int grid = wide_grid(b.nb / 2);
+  const size_t smem = (size_t)WCH * WLD * 8;
+  e = cudaFuncSetAttribute(wide_bjacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int grid = wide_grid(b.nb / 2, smem);
   void* args[] = {&b};
-  return cudaLaunchCooperativeKernel((void*)wide_bjacobi_kernel, grid, WT, args, 0, s);
+  return cudaLaunchCooperativeKernel((void*)wide_bjacobi_kernel, grid, WT, args, smem, s);
 }
 
 cudaError_t launch_jacobi_eig_wide(const double* B, int ldb, int n, double tol, double trunc, int max_sweeps,
