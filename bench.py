@@ -179,14 +179,15 @@ def run_reference(args, rank, world):
     import oracle
 
     cfg = synth.CONFIGS[args.config]
-    rows = args.cpu_sample_rows or (200_000 if cfg["kind"] == "tssvd" else 20_000)
+    rows = args.cpu_sample_rows or (min(200_000, max(10_000, int(2e11 / cfg["n"] ** 2)))
+                                     if cfg["kind"] == "tssvd" else 20_000)
     d = synth.config_inputs(args.config, m=min(rows, cfg["m"]),
                             n=None if cfg["kind"] == "tssvd" else min(cfg["n"], 4_000))
     a = d["A"]
 
     def step():
         if cfg["kind"] == "tssvd":
-            oracle.tssvd(a, args.wp, 2)
+            oracle.tssvd(a, cfg.get("wp", args.wp), 2)
         else:
             oracle.lowrank_svd(a, d["Omega"], d["iters"], d["k"], args.wp)
 
@@ -218,11 +219,14 @@ def metric_name(cfg):
 
 
 def config_obj(args, cfg, world):
+    paper = {"t3": "PAPER Table 3", "t4": "PAPER Table 4", "t5": "PAPER Table 5",
+             "s21": "PAPER Table 21 (Devil's staircase)"}.get(args.config)
     c = {"workload": f"{args.config}: {cfg['m']}x{cfg['n']} FP64 "
                      + ("tall-skinny SVD, Alg. 4 (two Gram passes)" if cfg["kind"] == "tssvd"
-                        else f"low-rank SVD Alg. 8, k={cfg['k']} l={cfg['l']} i={cfg['iters']}"),
+                        else f"low-rank SVD Alg. 8, k={cfg['k']} l={cfg['l']} i={cfg['iters']}")
+                     + (f", {paper} matrix (Eq. originalmat, DCT factors)" if paper else ""),
          "m": cfg["m"], "n": cfg["n"], "rows_per_gpu": -(-cfg["m"] // world),
-         "working_precision": args.wp, "parallelism": f"row-shard x{world}",
+         "working_precision": cfg.get("wp", args.wp), "parallelism": f"row-shard x{world}",
          "l2": "A is larger than L2 (126 MB) on every rank; no flush needed"}
     return c
 
@@ -250,10 +254,12 @@ def run_ours(args, rank, world, local_rank):
         Om = om_host.to(dev)
     U = torch.empty_like(A) if not lowrank else None
 
+    wp = cfg.get("wp", args.wp)  # the paper workloads fix their own (reading Q1)
+
     def step():
         if lowrank:
-            return tk.lowrank_svd(A, Om, cfg["iters"], cfg["k"], wp=args.wp, comm=comm)
-        return tk.tssvd(A, wp=args.wp, passes=2, comm=comm, U=U)
+            return tk.lowrank_svd(A, Om, cfg["iters"], cfg["k"], wp=wp, comm=comm)
+        return tk.tssvd(A, wp=wp, passes=2, comm=comm, U=U)
 
     def barrier():
         if world > 1:
@@ -307,10 +313,10 @@ def run_ours(args, rank, world, local_rank):
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s0.record(stream)
             if lowrank:
-                u_h, s_h, v_h = tk.lowrank_svd(a_host, om_host, cfg["iters"], cfg["k"], wp=args.wp,
+                u_h, s_h, v_h = tk.lowrank_svd(a_host, om_host, cfg["iters"], cfg["k"], wp=wp,
                                                comm=comm)
             else:
-                u_h, s_h, v_h = tk.tssvd(a_host, wp=args.wp, passes=2, comm=comm)
+                u_h, s_h, v_h = tk.tssvd(a_host, wp=wp, passes=2, comm=comm)
             s1.record(stream)
             s1.synchronize()
             if i >= ew:
@@ -358,7 +364,7 @@ def run_ours(args, rank, world, local_rank):
     if not lowrank and world == 1:
         ortho = {}
         for npass in (1, 2):
-            u1, s1_, _ = tk.tssvd(A, wp=args.wp, passes=npass, U=U)
+            u1, s1_, _ = tk.tssvd(A, wp=wp, passes=npass, U=U)
             g = u1.T @ u1
             ortho[f"pass{npass}"] = (g - torch.eye(g.shape[0], dtype=g.dtype, device=dev)).abs().max().item()
 
@@ -387,14 +393,17 @@ def cpu_baseline(args, cfg):
     """The oracle as it stands, on this host's cores, on a bounded sample (~10-30 s)."""
     import oracle
 
-    rows = args.cpu_sample_rows or (500_000 if cfg["kind"] == "tssvd" else 20_000)
+    # bounded sample: ~2e11 m n^2 for the tall-skinny configs (500,000 rows at n = 100,
+    # 50,000 at n = 2000), 20,000 x 4,000 for the low-rank ones
+    tall_rows = min(500_000, max(10_000, int(2e11 / cfg["n"] ** 2)))
+    rows = args.cpu_sample_rows or (tall_rows if cfg["kind"] == "tssvd" else 20_000)
     d = synth.config_inputs(args.config, m=min(rows, cfg["m"]),
                             n=None if cfg["kind"] == "tssvd" else min(cfg["n"], 4_000))
     a = d["A"]
     reps, t0, c0 = 0, time.perf_counter(), time.process_time()
     while True:
         if cfg["kind"] == "tssvd":
-            oracle.tssvd(a, args.wp, 2)
+            oracle.tssvd(a, cfg.get("wp", args.wp), 2)
         else:
             oracle.lowrank_svd(a, d["Omega"], d["iters"], d["k"], args.wp)
         reps += 1

@@ -151,20 +151,32 @@ def lowrank_test_matrix(m: int, n: int, r: int, sigma: np.ndarray, noise: float,
     return out
 
 
-def dct_columns(m: int, k: int) -> np.ndarray:
-    """First k columns of the m x m orthonormal DCT-II matrix C^T (column j = j-th cosine basis vector)."""
-    i = np.arange(m, dtype=np.float64)[:, None]
+def dct_columns(m: int, k: int, rows: tuple[int, int] | None = None) -> np.ndarray:
+    """First k columns of the m x m orthonormal DCT-II matrix C^T (column j = j-th cosine basis
+    vector); rows [r0, r1) only when given (row shards of the paper's matrices)."""
+    r0, r1 = rows if rows is not None else (0, m)
+    i = np.arange(r0, r1, dtype=np.float64)[:, None]
     j = np.arange(k, dtype=np.float64)[None, :]
     c = np.cos(np.pi * (2.0 * i + 1.0) * j / (2.0 * m)) * math.sqrt(2.0 / m)
     c[:, 0] = 1.0 / math.sqrt(m)
     return c
 
 
-def paper_test_matrix(m: int, n: int) -> tuple[np.ndarray, np.ndarray]:
+def paper_test_matrix(m: int, n: int, rows: tuple[int, int] | None = None) -> tuple[np.ndarray, np.ndarray]:
     """Eq. originalmat + testS: A = U Sigma V^*, DCT U, V; returns (A, sigma)."""
     s = spectrum("testS", n)
-    a = (dct_columns(m, n) * s[None, :]) @ dct_columns(n, n).T
-    return a, s
+    w = s[:, None] * dct_columns(n, n).T
+    r0, r1 = rows if rows is not None else (0, m)
+    out = np.empty((r1 - r0, n))
+    step = 65536
+
+    def mul(b0):
+        b1 = min(r1, b0 + step)
+        out[b0 - r0:b1 - r0] = dct_columns(m, n, (b0, b1)) @ w
+
+    with ThreadPoolExecutor(_threads()) as ex:
+        list(ex.map(mul, range(r0, r1, step)))
+    return out, s
 
 
 def paper_lowrank_test_matrix(m: int, n: int, l: int) -> tuple[np.ndarray, np.ndarray]:
@@ -188,11 +200,12 @@ def devils_staircase(k: int) -> np.ndarray:
     return np.sort(out)[::-1].copy()
 
 
-def paper_staircase_matrix(m: int, n: int) -> tuple[np.ndarray, np.ndarray]:
+def paper_staircase_matrix(m: int, n: int, rows: tuple[int, int] | None = None) -> tuple[np.ndarray, np.ndarray]:
     """Eq. originalmat with the Devil's-staircase spectrum (k = n):
     A = U Sigma V^*, U and V the DCT factors of Eq. originalmat; returns (A, sigma)."""
     s = devils_staircase(n)
-    a = (dct_columns(m, n) * s[None, :]) @ dct_columns(n, n).T
+    r0, r1 = rows if rows is not None else (0, m)
+    a = (dct_columns(m, n, (r0, r1)) * s[None, :]) @ dct_columns(n, n).T
     return a, s
 
 
@@ -216,6 +229,13 @@ CONFIGS = {
     "c4": dict(kind="tssvd", m=8_000_000, n=200, spec=("log", 12.0), seed=4, passes=2),
     "c5": dict(kind="lowrank", m=500_000, n=40_000, r=100, spec=("exp15",), noise=1e-8,
                k=50, l=60, iters=4, seed=5),
+    # the paper's own tall-skinny workloads: Eq. originalmat with DCT
+    # factors, n = 2000; t3/t4/t5 = Tables 3/4/5 (testS spectrum, Alg. 4 at the reading-Q1
+    # wp = 1e-12), s21 = Table 21 (Devil's staircase, wp = 1e-11)
+    "t3": dict(kind="tssvd", m=1_000_000, n=2_000, spec=("testS",), gen="dct", seed=0, passes=2, wp=1e-12),
+    "t4": dict(kind="tssvd", m=100_000, n=2_000, spec=("testS",), gen="dct", seed=0, passes=2, wp=1e-12),
+    "t5": dict(kind="tssvd", m=10_000, n=2_000, spec=("testS",), gen="dct", seed=0, passes=2, wp=1e-12),
+    "s21": dict(kind="tssvd", m=10_000, n=2_000, spec=("staircase",), gen="dct", seed=0, passes=2, wp=1e-11),
 }
 
 
@@ -237,7 +257,10 @@ def config_inputs(name: str, m: int | None = None, n: int | None = None,
     mm = m or cfg["m"]
     nn = n or cfg["n"]
     out = dict(name=name, m=mm, n=nn, cfg=cfg)
-    if cfg["kind"] == "tssvd":
+    if cfg.get("gen") == "dct":  # the paper's DCT-factor matrices
+        fn = paper_staircase_matrix if cfg["spec"][0] == "staircase" else paper_test_matrix
+        out["A"], out["sigma"] = fn(mm, nn, rows)
+    elif cfg["kind"] == "tssvd":
         sig = config_sigma(dict(cfg, n=nn))
         out["sigma"] = sig
         out["A"] = test_matrix(mm, nn, sig, cfg["seed"], rows)
