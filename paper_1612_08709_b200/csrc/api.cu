@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/tssvd.h"
 #include "common.cuh"
@@ -190,6 +191,10 @@ struct PassTimer {
     g_stats.n_pass = open + 1;
     open = -1;
   }
+  void create_all() {  // before a graph capture: no event creation inside it
+    for (auto& e : ev)
+      if (!e) CU(cudaEventCreate(&e));
+  }
   void resolve() {
     if (g_dry) return;
     for (int i = 0; i < g_stats.n_pass; ++i) {
@@ -298,18 +303,24 @@ struct Finish {
   int slots[8 * kMaxSlots];
   int64_t m = -1;
 };
-void finish(Ctx& c, Finish& f) {
+// the stream part of finish (guard allreduce, one D2H copy of the control block): a CUDA
+// graph of the call ends with it
+void finish_enqueue(Ctx& c) {
   step("finish");
-  if (g_dry) {
-    for (int q = 0; q < c.nslots; ++q) f.slots[8 * q] = f.slots[8 * q + 1] = 1 << 20;
-    return;
-  }
+  if (g_dry) return;
   if (c.dist() && c.nslots > 0) {
     CU(cudaMemcpyAsync(c.guard(), c.slots(), 8 * c.nslots * sizeof(int), cudaMemcpyDeviceToDevice, c.s));
     NC(ncclAllReduce(c.guard(), c.guard(), 8 * c.nslots, ncclInt32, ncclMax, c.comm->nccl, c.s));
   }
+  CU(cudaMemcpyAsync(host_ctl(), c.ctl, kCtlInts * sizeof(int), cudaMemcpyDeviceToHost, c.s));
+}
+
+void finish_host(Ctx& c, Finish& f) {
+  if (g_dry) {
+    for (int q = 0; q < c.nslots; ++q) f.slots[8 * q] = f.slots[8 * q + 1] = 1 << 20;
+    return;
+  }
   int* h = host_ctl();
-  CU(cudaMemcpyAsync(h, c.ctl, kCtlInts * sizeof(int), cudaMemcpyDeviceToHost, c.s));
   CU(cudaStreamSynchronize(c.s));
   std::memcpy(f.jinfo, h, sizeof f.jinfo);
   std::memcpy(f.slots, h + 8 * kMaxDeferred, sizeof f.slots);
@@ -326,6 +337,53 @@ void finish(Ctx& c, Finish& f) {
     if (f.slots[8 * q + kSlotBad]) fail(TSSVD_ENONFINITE, "non-finite entries in the input (A or Omega)");
   for (int q = 0; q < c.njinfo; ++q)
     if (!f.jinfo[8 * q + 1]) fail(TSSVD_ENOCONV, "Jacobi solve %d not converged in %d sweeps", q, f.jinfo[8 * q]);
+}
+
+void finish(Ctx& c, Finish& f) {
+  finish_enqueue(c);
+  finish_host(c, f);
+}
+
+// ---- one CUDA graph per call (the device-decision paths: lowrank_svd) -------------
+// With every decision on the device, a call is a fixed sequence of kernels, copies and
+// NCCL collectives for fixed arguments: it is captured once and replayed (TSSVD_GRAPH=0
+// disables).  The key is every argument that reaches a launch (pointers baked into kernel
+// parameters and TMA descriptors included); a replay restores the host-side counters the
+// capture produced.
+struct GraphKey {
+  const void* p[10];
+  int64_t v[10];
+  double wp;
+  bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof *this) == 0; }
+};
+struct GraphEntry {
+  GraphKey key;
+  cudaGraphExec_t exec = nullptr;
+  tssvd_stats stats;
+  int njinfo = 0, nslots = 0;
+  int aux[4] = {0, 0, 0, 0};  // call-specific host values the replay needs
+};
+thread_local std::vector<GraphEntry> g_graphs;
+constexpr size_t kMaxGraphs = 8;
+
+bool graphs_on() {
+  static const bool on = !getenv("TSSVD_GRAPH") || atoi(getenv("TSSVD_GRAPH")) != 0;
+  return on;
+}
+GraphEntry* graph_find(const GraphKey& k) {
+  for (auto& e : g_graphs)
+    if (e.key == k) return &e;
+  return nullptr;
+}
+GraphEntry* graph_store(const GraphKey& k, cudaGraphExec_t ex) {
+  if (g_graphs.size() >= kMaxGraphs) {
+    cudaGraphExecDestroy(g_graphs.front().exec);
+    g_graphs.erase(g_graphs.begin());
+  }
+  g_graphs.push_back(GraphEntry{});
+  g_graphs.back().key = k;
+  g_graphs.back().exec = ex;
+  return &g_graphs.back();
 }
 
 // One-sided Jacobi rotation threshold for columns of `rows` dot-product rows:
@@ -753,8 +811,8 @@ int64_t global_rows(Ctx& c, int64_t m_local) {
   if (!c.dist()) return m_local;
   step("allreduce:m:1");
   if (g_dry) return -1;
-  int64_t* h = reinterpret_cast<int64_t*>(host_ctl() + kCtlInts);  // own staging word (H2D in flight)
-  *h = m_local;
+  int64_t* h = reinterpret_cast<int64_t*>(host_ctl() + kCtlInts);  // own staging word (H2D in flight;
+  *h = m_local;                                                      // a graph replay restages it)
   CU(cudaMemcpyAsync(c.m64(), h, 8, cudaMemcpyHostToDevice, c.s));
   NC(ncclAllReduce(c.m64(), c.m64(), 1, ncclInt64, ncclSum, c.comm->nccl, c.s));
   return -1;
@@ -977,6 +1035,32 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
   LrPlan p;
   plan_lowrank(a, p, m_local, (int)n, (int)l, opts);
   c.ctl = p.ctl;
+  const bool use_graph = !hio && !g_dry && graphs_on();
+  GraphKey key{};
+  if (use_graph) {
+    const void* ps[10] = {comm, A, Omega, U, sigma, V, ws, stream, nullptr, nullptr};
+    const int64_t vs[10] = {m_local, n, lda, ldo, l, iters, k, ldu, ldv, (int64_t)ws_bytes ^ ((int64_t)opts->max_jacobi_sweeps << 48) ^ ((int64_t)g_timing << 60)};
+    std::memcpy(key.p, ps, sizeof ps);
+    std::memcpy(key.v, vs, sizeof vs);
+    key.wp = opts->working_precision;
+    host_ctl();  // pinned staging allocated outside any capture
+    if (g_timing) g_timer.create_all();
+    if (GraphEntry* e = graph_find(key)) {  // replay the captured call
+      if (c.dist()) *reinterpret_cast<int64_t*>(host_ctl() + kCtlInts) = m_local;
+      g_stats = e->stats;
+      c.njinfo = e->njinfo;
+      c.nslots = e->nslots;
+      CU(cudaGraphLaunch(e->exec, c.s));
+      Finish f;
+      finish_host(c, f);
+      if (c.dist() && l >= std::min<int64_t>(f.m, n)) fail(TSSVD_EINVAL, "need l < min(m, n) (P:705-707)");
+      *rank = std::min<int64_t>(e->aux[0], f.slots[8 * e->aux[1] + kSlotR]);
+      g_timer.resolve();
+      return;
+    }
+    CU(cudaStreamBeginCapture(c.s, cudaStreamCaptureModeThreadLocal));
+  }
+  try {
   step("lowrank:%d:%lld:%lld", iters, (long long)l, (long long)k);
   CUR(cudaMemsetAsync(c.ctl, 0, kCtlInts * sizeof(int), c.s));
   const int64_t m_now = global_rows(c, m_local);
@@ -1043,8 +1127,24 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
   const int64_t ldvo = hio ? kk : ldv;
   KS(copy2d(p.sig_tmp, kk, So, kk, 1, kk, c.s));
   KS(copy2d(p.Z, ldz, Vo, ldvo, N, kk, c.s));
+  finish_enqueue(c);
+  if (use_graph) {  // end of the capture: instantiate, keep, launch
+    cudaGraph_t gr = nullptr;
+    CU(cudaStreamEndCapture(c.s, &gr));
+    cudaGraphExec_t ex = nullptr;
+    const cudaError_t ie = cudaGraphInstantiate(&ex, gr, 0);
+    cudaGraphDestroy(gr);
+    CU(ie);
+    GraphEntry* e = graph_store(key, ex);
+    e->stats = g_stats;
+    e->njinfo = c.njinfo;
+    e->nslots = c.nslots;
+    e->aux[0] = kk;
+    e->aux[1] = o4.slot;
+    CU(cudaGraphLaunch(ex, c.s));
+  }
   Finish f;
-  finish(c, f);
+  finish_host(c, f);
   if (c.dist() && !g_dry && l >= std::min<int64_t>(f.m, n)) fail(TSSVD_EINVAL, "need l < min(m, n) (P:705-707)");
   const int r = (int)std::min<int64_t>(kk, core_rank(o4, f));
   if (hio && r > 0) {
@@ -1057,6 +1157,18 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
   }
   g_timer.resolve();
   *rank = r;
+  } catch (...) {
+    if (use_graph) {  // a failure inside the capture: end it (the stream leaves capture mode)
+      cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+      if (cudaStreamIsCapturing(c.s, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone) {
+        cudaGraph_t gr = nullptr;
+        cudaStreamEndCapture(c.s, &gr);
+        if (gr) cudaGraphDestroy(gr);
+      }
+      cudaGetLastError();
+    }
+    throw;
+  }
 }
 
 }  // namespace

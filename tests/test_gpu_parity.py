@@ -228,7 +228,7 @@ def test_tssvd_zero_matrix_and_errors():
     with pytest.raises(TssvdError, match="EINVAL"):
         tk.tssvd(torch.ones((8, 10), dtype=torch.float64, device=DEV))  # wide
     with pytest.raises(TssvdError, match="EINVAL"):
-        tk.sym_eig(torch.eye(300, dtype=torch.float64, device=DEV))  # n > 256: EINVAL, not ECUDA
+        tk.sym_eig(torch.eye(2050, dtype=torch.float64, device=DEV))  # n > 2048: EINVAL, not ECUDA
 
 
 def test_tssvd_host_io_matches_device():
