@@ -1058,6 +1058,11 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
       g_timer.resolve();
       return;
     }
+    // capture on a library-owned stream (the caller's may be the legacy default stream,
+    // which cannot be captured); the graph is launched on the caller's stream
+    static thread_local cudaStream_t cap = nullptr;
+    if (!cap) CU(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    c.s = cap;
     CU(cudaStreamBeginCapture(c.s, cudaStreamCaptureModeThreadLocal));
   }
   try {
@@ -1141,6 +1146,7 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
     e->nslots = c.nslots;
     e->aux[0] = kk;
     e->aux[1] = o4.slot;
+    c.s = static_cast<cudaStream_t>(stream);
     CU(cudaGraphLaunch(ex, c.s));
   }
   Finish f;
@@ -1166,6 +1172,7 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
         if (gr) cudaGraphDestroy(gr);
       }
       cudaGetLastError();
+      c.s = static_cast<cudaStream_t>(stream);
     }
     throw;
   }
