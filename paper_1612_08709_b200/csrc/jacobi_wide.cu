@@ -228,115 +228,150 @@ struct BjArgs {
   int L;      // rows per column (dot rows + accumulator rows)
   int dot;    // rows entering the Gram
   int nb;     // blocks (even), columns = nb * 16
+  int S;      // CTAs per job (row split)
   double tol2, skip2;
   int max_sweeps;
+  double* gpart;  // [njobs * S][32 * 32] partial Grams
   int* flag;  // [2] rotation flags per sweep parity
   int* info;  // info[0] sweeps, info[1] converged
 };
 
+// Each job (block pair) is shared by S CTAs that split its rows: phase 1, every CTA forms the
+// partial 32 x 32 Gram of its dot rows (DMMA) into global memory; grid barrier; phase 2,
+// every CTA of the job sums the S partials in part order (bit-identical on all of them),
+// runs the same inner sweep, and applies W to its own rows; grid barrier.
 __global__ void __launch_bounds__(WT, 1) wide_bjacobi_kernel(const BjArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double Ys[];  // [WCH * WLD]
-  __shared__ double Gs[WPC][WPC + 1];
-  __shared__ double Ws[WPC][WLD];
+  __shared__ double Gs[2][WPC][WPC + 1];
+  __shared__ double Ws[WPC][WPC + 1];
+  __shared__ double s_c[WPC / 2], s_s[WPC / 2];
   __shared__ int s_any;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-  const int nb = a.nb, njobs = nb / 2;
+  const int nb = a.nb, njobs = nb / 2, S = a.S, units = njobs * S;
   int sweep = 0;
   bool converged = false;
   for (; sweep < a.max_sweeps; ++sweep) {
     if (blockIdx.x == 0 && tid == 0) a.flag[(sweep + 1) & 1] = 0;
     for (int r = 0; r < nb - 1; ++r) {
-      for (int job = blockIdx.x; job < njobs; job += gridDim.x) {
+      // ---------------- phase 1: partial Grams
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int job = u / S, part = u % S;
         const int bp = job ? 1 + (job - 1 + r) % (nb - 1) : 0;
         const int bq = 1 + (nb - 2 - job + r) % (nb - 1);
-        // column c of the job (0..31) -> global column
         auto gcol = [&](int c) { return (c < WBS ? bp * WBS + c : bq * WBS + c - WBS); };
-        // chunk loader: element q of thread tid -> (column c, chunk row rr); the next chunk is
-        // loaded into registers while the current one is consumed (one L2 round trip in flight)
-        auto load = [&](int r0, int lim, double (&v)[WPER]) {
-#pragma unroll
-          for (int q = 0; q < WPER; ++q) {
-            const int e = tid + q * WT, c = e / WCH, rr = e % WCH, row = r0 + rr;
-            v[q] = row < lim ? __ldcg(a.C + (size_t)gcol(c) * a.ldc + row) : 0.0;
-          }
-        };
-        auto stage = [&](const double (&v)[WPER]) {
-#pragma unroll
-          for (int q = 0; q < WPER; ++q) {
-            const int e = tid + q * WT;
-            Ys[(e % WCH) * WLD + e / WCH] = v[q];
-          }
-        };
-        // ---- A. Gram of the 32 columns over the dot rows (DMMA; warp w: tile (w/4, w%4))
+        const int lo = (int)((int64_t)a.dot * part / S), hi = (int)((int64_t)a.dot * (part + 1) / S);
         const int ti = warp >> 2, tj = warp & 3;
         double acc[2] = {0.0, 0.0};
         double cur[WPER], nxt[WPER];
-        load(0, a.dot, cur);
-        for (int r0 = 0; r0 < a.dot; r0 += WCH) {
-          stage(cur);
-          __syncthreads();
-          if (r0 + WCH < a.dot) load(r0 + WCH, a.dot, nxt);
-#pragma unroll 4
-          for (int kk = 0; kk < WCH / 4; ++kk) {
-            const double fa = Ys[(kk * 4 + t) * WLD + ti * 8 + g];
-            const double fb = Ys[(kk * 4 + t) * WLD + tj * 8 + g];
-            dmma(acc, fa, fb);
+        auto load = [&](int r0, double (&v)[WPER]) {
+#pragma unroll
+          for (int q = 0; q < WPER; ++q) {
+            const int e = tid + q * WT, c = e / WCH, rr = e % WCH, row = r0 + rr;
+            v[q] = row < hi ? __ldcg(a.C + (size_t)gcol(c) * a.ldc + row) : 0.0;
           }
+        };
+        if (lo < hi) load(lo, cur);
+        for (int r0 = lo; r0 < hi; r0 += WCH) {
+#pragma unroll
+          for (int q = 0; q < WPER; ++q) {
+            const int e = tid + q * WT;
+            Ys[(e % WCH) * WLD + e / WCH] = cur[q];
+          }
+          __syncthreads();
+          if (r0 + WCH < hi) load(r0 + WCH, nxt);
+#pragma unroll 4
+          for (int kk = 0; kk < WCH / 4; ++kk)
+            dmma(acc, Ys[(kk * 4 + t) * WLD + ti * 8 + g], Ys[(kk * 4 + t) * WLD + tj * 8 + g]);
           __syncthreads();
 #pragma unroll
           for (int q = 0; q < WPER; ++q) cur[q] = nxt[q];
         }
-        Gs[ti * 8 + g][tj * 8 + 2 * t] = acc[0];
-        Gs[ti * 8 + g][tj * 8 + 2 * t + 1] = acc[1];
-        for (int e = tid; e < WPC * WPC; e += WT) Ws[e / WPC][e % WPC] = (e / WPC == e % WPC) ? 1.0 : 0.0;
+        double* gp = a.gpart + (size_t)u * WPC * WPC;
+        gp[(ti * 8 + g) * WPC + tj * 8 + 2 * t] = acc[0];
+        gp[(ti * 8 + g) * WPC + tj * 8 + 2 * t + 1] = acc[1];
+      }
+      grid.sync();
+      // ---------------- phase 2: sum, test, inner sweep, apply to the own rows
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int job = u / S, part = u % S;
+        const int bp = job ? 1 + (job - 1 + r) % (nb - 1) : 0;
+        const int bq = 1 + (nb - 2 - job + r) % (nb - 1);
+        auto gcol = [&](int c) { return (c < WBS ? bp * WBS + c : bq * WBS + c - WBS); };
+        for (int e = tid; e < WPC * WPC; e += WT) {
+          double v = 0.0;
+          for (int q = 0; q < S; ++q) v += __ldcg(a.gpart + ((size_t)(job * S + q) * WPC * WPC) + e);
+          Gs[0][e / WPC][e % WPC] = v;
+          Ws[e / WPC][e % WPC] = (e / WPC == e % WPC) ? 1.0 : 0.0;
+        }
         if (tid == 0) s_any = 0;
         __syncthreads();
-        // ---- B. any pair above the rotation threshold?
         {
           int need = 0;
           for (int e = tid; e < WPC * WPC; e += WT) {
             const int i = e / WPC, j = e % WPC;
             if (i < j) {
-              const double al = Gs[i][i], be = Gs[j][j], ga = Gs[i][j];
+              const double al = Gs[0][i][i], be = Gs[0][j][j], ga = Gs[0][i][j];
               need |= (ga != 0.0 && ga * ga > a.tol2 * al * be && fmax(al, be) > a.skip2);
             }
           }
-          if (__syncthreads_or(need)) {
-            if (tid == 0) {
-              s_any = 1;
-              atomicOr(a.flag + (sweep & 1), 1);
-            }
+          if (__syncthreads_or(need) && tid == 0) {
+            s_any = 1;
+            if (part == 0) atomicOr(a.flag + (sweep & 1), 1);
           }
         }
         __syncthreads();
-        if (!s_any) continue;  // uniform over the CTA
-        // ---- C. one sweep of two-sided Jacobi on Gs (circle ordering over 32 indices),
-        // W accumulates the rotations; warp w rotates pair w of the round
+        if (!s_any) continue;  // uniform over the CTA (and over the job's S CTAs)
+        // inner sweep: circle ordering over 32 indices, 16 disjoint rotations per round;
+        // (a) warp k computes pair k's rotation from the current G; (b) thread (i, k) forms
+        // rows i of G' = J^T G J at columns p_k, q_k (double-buffered G) and W's (i, p_k), (i, q_k)
+        int cb = 0;
+        const int ui = tid >> 4, uk = tid & 15;  // update role: row ui, pair uk
         for (int rr = 0; rr < WPC - 1; ++rr) {
-          const int p = warp ? 1 + (warp - 1 + rr) % (WPC - 1) : 0;
-          const int q = 1 + (WPC - 2 - warp + rr) % (WPC - 1);
-          double c = 1.0, sn = 0.0;
-          const bool rot = wide_rot(Gs[p][p], Gs[q][q], Gs[p][q], a.tol2, a.skip2, c, sn);
-          __syncthreads();  // every warp has read its 2 x 2 block
-          if (rot) {  // rows p, q
-            const double gp = Gs[p][lane], gq = Gs[q][lane];
-            Gs[p][lane] = fma(c, gp, -sn * gq);
-            Gs[q][lane] = fma(sn, gp, c * gq);
+          auto pair_p = [&](int k) { return k ? 1 + (k - 1 + rr) % (WPC - 1) : 0; };
+          auto pair_q = [&](int k) { return 1 + (WPC - 2 - k + rr) % (WPC - 1); };
+          {
+            const int p = pair_p(warp), q = pair_q(warp);
+            double c = 1.0, sn = 0.0;
+            wide_rot(Gs[cb][p][p], Gs[cb][q][q], Gs[cb][p][q], a.tol2, a.skip2, c, sn);
+            if (lane == 0) s_c[warp] = c, s_s[warp] = sn;
           }
           __syncthreads();
-          if (rot) {  // columns p, q of G and W
-            const double gp = Gs[lane][p], gq = Gs[lane][q];
-            Gs[lane][p] = fma(c, gp, -sn * gq);
-            Gs[lane][q] = fma(sn, gp, c * gq);
-            const double wp = Ws[lane][p], wq = Ws[lane][q];
-            Ws[lane][p] = fma(c, wp, -sn * wq);
-            Ws[lane][q] = fma(sn, wp, c * wq);
+          {
+            const int p = pair_p(uk), q = pair_q(uk);
+            const double c = s_c[uk], sn = s_s[uk];
+            // the pair of row ui: (pi, qi), and whether ui is its p
+            int ki = 0;
+            for (int k = 0; k < WPC / 2; ++k)
+              if (pair_p(k) == ui || pair_q(k) == ui) ki = k;
+            const int pi = pair_p(ki), qi = pair_q(ki);
+            const int oth = ui == pi ? qi : pi;
+            const double ci = s_c[ki], si = s_s[ki];
+            // (G J)[x][p], (G J)[x][q] for x = ui, oth
+            const double gup = fma(c, Gs[cb][ui][p], -sn * Gs[cb][ui][q]);
+            const double guq = fma(sn, Gs[cb][ui][p], c * Gs[cb][ui][q]);
+            const double gop = fma(c, Gs[cb][oth][p], -sn * Gs[cb][oth][q]);
+            const double goq = fma(sn, Gs[cb][oth][p], c * Gs[cb][oth][q]);
+            // row ui of J^T (G J): ui = p_i: c_i row(p_i) - s_i row(q_i); ui = q_i: s_i row(p_i) + c_i row(q_i)
+            double np, nq;
+            if (ui == pi) {
+              np = fma(ci, gup, -si * gop);
+              nq = fma(ci, guq, -si * goq);
+            } else {
+              np = fma(si, gop, ci * gup);
+              nq = fma(si, goq, ci * guq);
+            }
+            Gs[cb ^ 1][ui][p] = np;
+            Gs[cb ^ 1][ui][q] = nq;
+            const double wp = Ws[ui][p], wq = Ws[ui][q];
+            Ws[ui][p] = fma(c, wp, -sn * wq);
+            Ws[ui][q] = fma(sn, wp, c * wq);
           }
-          __syncthreads();  // the next round reads 2 x 2 blocks this column phase wrote
+          __syncthreads();
+          cb ^= 1;
         }
-        // W's columns back to unit norm: each rotation's c^2 + s^2 is 1 only to a few ulp, and
-        // over ~(blocks x sweeps) applications per column that norm drift (not the mutual
+        // W's columns back to unit norm: each rotation's c^2 + s^2 is 1 only to a few ulp,
+        // and over ~(blocks x sweeps) applications per column that norm drift (not the mutual
         // orthogonality, which drifts at second order) made Y Y^T wander from B by ~1e-13
         // relative on the paper's n = 2000 staircase (measured); one normalisation per job
         // keeps every applied W orthogonal to rounding.
@@ -346,15 +381,29 @@ __global__ void __launch_bounds__(WT, 1) wide_bjacobi_kernel(const BjArgs a) {
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) s0 += __shfl_xor_sync(0xffffffffu, s0, o), s1 += __shfl_xor_sync(0xffffffffu, s1, o);
           const double i0 = rsqrt_nr_w(s0), i1 = rsqrt_nr_w(s1);
+          __syncthreads();
           for (int i = lane; i < WPC; i += 32) Ws[i][2 * warp] *= i0, Ws[i][2 * warp + 1] *= i1;
         }
         __syncthreads();
-        // ---- D. Y <- Y W over all rows (DMMA; chunk 128 x 32 = 16 x 4 tiles, 4 per warp)
-        load(0, a.L, cur);
-        for (int r0 = 0; r0 < a.L; r0 += WCH) {
-          stage(cur);
+        // Y <- Y W on the own rows [lo, hi) of all L rows (DMMA; chunk 128 x 32, 4 tiles per warp)
+        const int lo = (int)((int64_t)a.L * part / S), hi = (int)((int64_t)a.L * (part + 1) / S);
+        double cur[WPER], nxt[WPER];
+        auto load = [&](int r0, double (&v)[WPER]) {
+#pragma unroll
+          for (int q = 0; q < WPER; ++q) {
+            const int e = tid + q * WT, c = e / WCH, rr = e % WCH, row = r0 + rr;
+            v[q] = row < hi ? __ldcg(a.C + (size_t)gcol(c) * a.ldc + row) : 0.0;
+          }
+        };
+        if (lo < hi) load(lo, cur);
+        for (int r0 = lo; r0 < hi; r0 += WCH) {
+#pragma unroll
+          for (int q = 0; q < WPER; ++q) {
+            const int e = tid + q * WT;
+            Ys[(e % WCH) * WLD + e / WCH] = cur[q];
+          }
           __syncthreads();
-          if (r0 + WCH < a.L) load(r0 + WCH, a.L, nxt);
+          if (r0 + WCH < hi) load(r0 + WCH, nxt);
 #pragma unroll
           for (int h = 0; h < WCH / 32; ++h) {
             const int tile = warp * (WCH / 32) + h, bi = tile >> 2, bj = tile & 3;
@@ -363,7 +412,7 @@ __global__ void __launch_bounds__(WT, 1) wide_bjacobi_kernel(const BjArgs a) {
             for (int kk = 0; kk < WPC / 4; ++kk)
               dmma(o, Ys[(bi * 8 + g) * WLD + kk * 4 + t], Ws[kk * 4 + t][bj * 8 + g]);
             const int row = r0 + bi * 8 + g;
-            if (row < a.L) {
+            if (row < hi) {
               a.C[(size_t)gcol(bj * 8 + 2 * t) * a.ldc + row] = o[0];
               a.C[(size_t)gcol(bj * 8 + 2 * t + 1) * a.ldc + row] = o[1];
             }
@@ -454,11 +503,13 @@ size_t jacobi_wide_workspace(int n, int L) {
   return (size_t)n * n          // X row-major (EIG)
          + (size_t)kmax * ldc   // columns
          + (size_t)kmax         // norms
-         + 4 * 256 + 64;        // candidates, flags, K
+         + 4 * 256 + 64         // candidates, flags, K
+         + 1024                 // (int area)
+         + (size_t)256 * 1024;  // partial Grams of the row-split jobs
 }
 
 static cudaError_t run_sweeps(double* C, int ldc, int L, int dot, int kmax, double tol, int max_sweeps,
-                              int* flag, int* info, cudaStream_t s) {
+                              int* flag, int* info, double* gpart, cudaStream_t s) {
   BjArgs b{};
   b.C = C;
   b.ldc = ldc;
@@ -475,12 +526,16 @@ static cudaError_t run_sweeps(double* C, int ldc, int L, int dot, int kmax, doub
   b.max_sweeps = max_sweeps;
   b.flag = flag;
   b.info = info;
+  b.gpart = gpart;
   cudaError_t e = cudaMemsetAsync(flag, 0, 2 * sizeof(int), s);
   if (e != cudaSuccess) return e;
   const size_t smem = (size_t)WCH * WLD * 8;
   e = cudaFuncSetAttribute(wide_bjacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const int grid = wide_grid(b.nb / 2, smem);
+  // CTAs per job: as many as keep every job's CTAs co-resident (the row split)
+  const int cap = wide_grid(1 << 20, smem);
+  b.S = std::max(1, std::min(8, cap / std::max(1, b.nb / 2)));
+  const int grid = std::max(1, std::min(cap, (b.nb / 2) * b.S));
   void* args[] = {&b};
   return cudaLaunchCooperativeKernel((void*)wide_bjacobi_kernel, grid, WT, args, smem, s);
 }
@@ -522,7 +577,7 @@ cudaError_t launch_jacobi_eig_wide(const double* B, int ldb, int n, double tol, 
   e = cudaLaunchCooperativeKernel((void*)wide_pchol_kernel, rows_grid, WT, pargs, smem, s);
   if (e != cudaSuccess) return e;
   wide_to_cols<<<(unsigned)(((int64_t)kmax * ldc + 255) / 256), 256, 0, s>>>(X, n, Kp, kmax, C, ldc);
-  e = run_sweeps(C, ldc, n, n, kmax, tol, max_sweeps, flag, info, s);
+  e = run_sweeps(C, ldc, n, n, kmax, tol, max_sweeps, flag, info, cval + 2 * 256 + 1024, s);
   if (e != cudaSuccess) return e;
   wide_norms<<<kmax, 256, 0, s>>>(C, ldc, n, kmax, nrm);
   wide_output<<<kmax, 256, 0, s>>>(C, ldc, n, n, n, kmax, Kp, nrm, 0, n, vecs, ldv, vals);
@@ -557,7 +612,7 @@ cudaError_t launch_jacobi_svd_wide(const double* cols, int ldc_in, int N, int do
   wide_set_int<<<1, 1, 0, s>>>(Kp, N);
   wide_load_svd<<<(unsigned)(((int64_t)kmax * ldc + 255) / 256), 256, 0, s>>>(cols, ldc_in, N, dot, dpad, kmax, C,
                                                                              ldc);
-  e = run_sweeps(C, ldc, L, dot, kmax, tol, max_sweeps, flag, info, s);
+  e = run_sweeps(C, ldc, L, dot, kmax, tol, max_sweeps, flag, info, cval + 2 * 256 + 1024, s);
   if (e != cudaSuccess) return e;
   wide_norms<<<kmax, 256, 0, s>>>(C, ldc, dot, kmax, nrm);
   wide_output<<<kmax, 256, 0, s>>>(C, ldc, L, dot, dpad, kmax, Kp, nrm, 1, N, out, ldout, vals);
