@@ -222,6 +222,15 @@ __global__ void wide_load_svd(const double* in, int ldin, int N, int dot, int dp
 }
 
 // --------------------------------------------------- 2. block Jacobi sweeps --
+#ifdef WIDE_PROF  // phase timing of the block sweeps (A/B builds only: tools/wide_prof.py)
+__device__ unsigned long long g_wide_phase[8];
+#define WP_T(i) long long wp_t##i = (blockIdx.x == 0 && threadIdx.x == 0) ? clock64() : 0;
+#define WP_ACC(k, a, b) if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&g_wide_phase[k], (unsigned long long)(wp_t##b - wp_t##a));
+#else
+#define WP_T(i)
+#define WP_ACC(k, a, b)
+#endif
+
 struct BjArgs {
   double* C;  // columns, ld ldc
   int ldc;
@@ -254,6 +263,7 @@ __global__ void __launch_bounds__(WT, 1) wide_bjacobi_kernel(const BjArgs a) {
   for (; sweep < a.max_sweeps; ++sweep) {
     if (blockIdx.x == 0 && tid == 0) a.flag[(sweep + 1) & 1] = 0;
     for (int r = 0; r < nb - 1; ++r) {
+      WP_T(0)
       // ---------------- phase 1: partial Grams
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const int job = u / S, part = u % S;
@@ -291,7 +301,11 @@ __global__ void __launch_bounds__(WT, 1) wide_bjacobi_kernel(const BjArgs a) {
         gp[(ti * 8 + g) * WPC + tj * 8 + 2 * t] = acc[0];
         gp[(ti * 8 + g) * WPC + tj * 8 + 2 * t + 1] = acc[1];
       }
+      WP_T(1)
       grid.sync();
+      WP_T(2)
+      WP_ACC(0, 0, 1)
+      WP_ACC(1, 1, 2)
       // ---------------- phase 2: sum, test, inner sweep, apply to the own rows
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         const int job = u / S, part = u % S;
@@ -321,6 +335,8 @@ __global__ void __launch_bounds__(WT, 1) wide_bjacobi_kernel(const BjArgs a) {
           }
         }
         __syncthreads();
+        WP_T(3)
+        WP_ACC(2, 2, 3)
         if (!s_any) continue;  // uniform over the CTA (and over the job's S CTAs)
         // inner sweep: circle ordering over 32 indices, 16 disjoint rotations per round;
         // (a) warp k computes pair k's rotation from the current G; (b) thread (i, k) forms
@@ -385,6 +401,8 @@ __global__ void __launch_bounds__(WT, 1) wide_bjacobi_kernel(const BjArgs a) {
           for (int i = lane; i < WPC; i += 32) Ws[i][2 * warp] *= i0, Ws[i][2 * warp + 1] *= i1;
         }
         __syncthreads();
+        WP_T(4)
+        WP_ACC(3, 3, 4)
         // Y <- Y W on the own rows [lo, hi) of all L rows (DMMA; chunk 128 x 32, 4 tiles per warp)
         const int lo = (int)((int64_t)a.L * part / S), hi = (int)((int64_t)a.L * (part + 1) / S);
         double cur[WPER], nxt[WPER];
@@ -421,8 +439,13 @@ __global__ void __launch_bounds__(WT, 1) wide_bjacobi_kernel(const BjArgs a) {
 #pragma unroll
           for (int q = 0; q < WPER; ++q) cur[q] = nxt[q];
         }
+        WP_T(5)
+        WP_ACC(4, 4, 5)
       }
+      WP_T(6)
       grid.sync();
+      WP_T(7)
+      WP_ACC(5, 6, 7)
     }
     // end of the sweep: did any job rotate?
     const int any = __ldcg(a.flag + (sweep & 1));
@@ -534,11 +557,20 @@ static cudaError_t run_sweeps(double* C, int ldc, int L, int dot, int kmax, doub
   if (e != cudaSuccess) return e;
   // CTAs per job: as many as keep every job's CTAs co-resident (the row split)
   const int cap = wide_grid(1 << 20, smem);
-  b.S = std::max(1, std::min(8, cap / std::max(1, b.nb / 2)));
+  static const int force_s = getenv("TSSVD_WIDE_S") ? atoi(getenv("TSSVD_WIDE_S")) : 0;
+  b.S = force_s > 0 ? force_s : std::max(1, std::min(8, cap / std::max(1, b.nb / 2)));
   const int grid = std::max(1, std::min(cap, (b.nb / 2) * b.S));
   void* args[] = {&b};
   return cudaLaunchCooperativeKernel((void*)wide_bjacobi_kernel, grid, WT, args, smem, s);
 }
+
+#ifdef WIDE_PROF
+extern "C" int tssvd_wide_prof(unsigned long long* out) {  // read and reset the phase counters
+  if (cudaMemcpyFromSymbol(out, g_wide_phase, sizeof(unsigned long long) * 8) != cudaSuccess) return 1;
+  unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  return cudaMemcpyToSymbol(g_wide_phase, z, sizeof z) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 cudaError_t launch_jacobi_eig_wide(const double* B, int ldb, int n, double tol, double trunc, int max_sweeps,
                                    double* vecs, int ldv, double* vals, int* info, double* work,
