@@ -254,10 +254,21 @@ __global__ void __launch_bounds__(WT, 1) wide_bjacobi_kernel(const BjArgs a) {
   extern __shared__ __align__(16) double Ys[];  // [WCH * WLD]
   __shared__ double Gs[2][WPC][WPC + 1];
   __shared__ double Ws[WPC][WPC + 1];
-  __shared__ double s_c[WPC / 2], s_s[WPC / 2];
+  __shared__ unsigned char s_pp[WPC - 1][WPC / 2], s_qq[WPC - 1][WPC / 2], s_pos[WPC - 1][WPC];
   __shared__ int s_any;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int nb = a.nb, njobs = nb / 2, S = a.S, units = njobs * S;
+  // the inner sweep's circle ordering, once: pair k of round rr = (s_pp, s_qq); s_pos[rr][i] =
+  // the pair of index i (+16 when i is its q)
+  for (int e = tid; e < (WPC - 1) * (WPC / 2); e += WT) {
+    const int rr = e / (WPC / 2), k = e % (WPC / 2);
+    const int p = k ? 1 + (k - 1 + rr) % (WPC - 1) : 0, q = 1 + (WPC - 2 - k + rr) % (WPC - 1);
+    s_pp[rr][k] = (unsigned char)p;
+    s_qq[rr][k] = (unsigned char)q;
+    s_pos[rr][p] = (unsigned char)k;
+    s_pos[rr][q] = (unsigned char)(k + 16);
+  }
+  __syncthreads();
   int sweep = 0;
   bool converged = false;
   for (; sweep < a.max_sweeps; ++sweep) {
@@ -338,51 +349,44 @@ __global__ void __launch_bounds__(WT, 1) wide_bjacobi_kernel(const BjArgs a) {
         WP_T(3)
         WP_ACC(2, 2, 3)
         if (!s_any) continue;  // uniform over the CTA (and over the job's S CTAs)
-        // inner sweep: circle ordering over 32 indices, 16 disjoint rotations per round;
-        // (a) warp k computes pair k's rotation from the current G; (b) thread (i, k) forms
-        // rows i of G' = J^T G J at columns p_k, q_k (double-buffered G) and W's (i, p_k), (i, q_k)
+        // inner sweep: circle ordering over 32 indices, 16 disjoint rotations per round.  Every
+        // warp computes all 16 rotations of the round (lane k: pair k mod 16) from the current
+        // G, so thread (i, k) gets its parameters by shuffles, forms row i of G' = J^T G J at
+        // columns p_k, q_k (double-buffered G) and W's (i, p_k), (i, q_k): one barrier per round.
+        // (The pair of index i in round rr comes from the precomputed table s_pos.)
         int cb = 0;
         const int ui = tid >> 4, uk = tid & 15;  // update role: row ui, pair uk
         for (int rr = 0; rr < WPC - 1; ++rr) {
-          auto pair_p = [&](int k) { return k ? 1 + (k - 1 + rr) % (WPC - 1) : 0; };
-          auto pair_q = [&](int k) { return 1 + (WPC - 2 - k + rr) % (WPC - 1); };
-          {
-            const int p = pair_p(warp), q = pair_q(warp);
-            double c = 1.0, sn = 0.0;
-            wide_rot(Gs[cb][p][p], Gs[cb][q][q], Gs[cb][p][q], a.tol2, a.skip2, c, sn);
-            if (lane == 0) s_c[warp] = c, s_s[warp] = sn;
+          const int mk = lane & 15;
+          const int mp = s_pp[rr][mk], mq = s_qq[rr][mk];
+          double mc = 1.0, ms = 0.0;
+          wide_rot(Gs[cb][mp][mp], Gs[cb][mq][mq], Gs[cb][mp][mq], a.tol2, a.skip2, mc, ms);
+          const int p = s_pp[rr][uk], q = s_qq[rr][uk];
+          const int pos = s_pos[rr][ui];
+          const int ki = pos & 15;
+          const bool is_p = pos < 16;
+          const int oth = is_p ? s_qq[rr][ki] : s_pp[rr][ki];
+          const double c = __shfl_sync(0xffffffffu, mc, uk), sn = __shfl_sync(0xffffffffu, ms, uk);
+          const double ci = __shfl_sync(0xffffffffu, mc, ki), si = __shfl_sync(0xffffffffu, ms, ki);
+          // (G J)[x][p], (G J)[x][q] for x = ui, oth
+          const double gup = fma(c, Gs[cb][ui][p], -sn * Gs[cb][ui][q]);
+          const double guq = fma(sn, Gs[cb][ui][p], c * Gs[cb][ui][q]);
+          const double gop = fma(c, Gs[cb][oth][p], -sn * Gs[cb][oth][q]);
+          const double goq = fma(sn, Gs[cb][oth][p], c * Gs[cb][oth][q]);
+          // row ui of J^T (G J): ui = p_i: c_i row(p_i) - s_i row(q_i); ui = q_i: s_i row(p_i) + c_i row(q_i)
+          double np, nq;
+          if (is_p) {
+            np = fma(ci, gup, -si * gop);
+            nq = fma(ci, guq, -si * goq);
+          } else {
+            np = fma(si, gop, ci * gup);
+            nq = fma(si, goq, ci * guq);
           }
-          __syncthreads();
-          {
-            const int p = pair_p(uk), q = pair_q(uk);
-            const double c = s_c[uk], sn = s_s[uk];
-            // the pair of row ui: (pi, qi), and whether ui is its p
-            int ki = 0;
-            for (int k = 0; k < WPC / 2; ++k)
-              if (pair_p(k) == ui || pair_q(k) == ui) ki = k;
-            const int pi = pair_p(ki), qi = pair_q(ki);
-            const int oth = ui == pi ? qi : pi;
-            const double ci = s_c[ki], si = s_s[ki];
-            // (G J)[x][p], (G J)[x][q] for x = ui, oth
-            const double gup = fma(c, Gs[cb][ui][p], -sn * Gs[cb][ui][q]);
-            const double guq = fma(sn, Gs[cb][ui][p], c * Gs[cb][ui][q]);
-            const double gop = fma(c, Gs[cb][oth][p], -sn * Gs[cb][oth][q]);
-            const double goq = fma(sn, Gs[cb][oth][p], c * Gs[cb][oth][q]);
-            // row ui of J^T (G J): ui = p_i: c_i row(p_i) - s_i row(q_i); ui = q_i: s_i row(p_i) + c_i row(q_i)
-            double np, nq;
-            if (ui == pi) {
-              np = fma(ci, gup, -si * gop);
-              nq = fma(ci, guq, -si * goq);
-            } else {
-              np = fma(si, gop, ci * gup);
-              nq = fma(si, goq, ci * guq);
-            }
-            Gs[cb ^ 1][ui][p] = np;
-            Gs[cb ^ 1][ui][q] = nq;
-            const double wp = Ws[ui][p], wq = Ws[ui][q];
-            Ws[ui][p] = fma(c, wp, -sn * wq);
-            Ws[ui][q] = fma(sn, wp, c * wq);
-          }
+          Gs[cb ^ 1][ui][p] = np;
+          Gs[cb ^ 1][ui][q] = nq;
+          const double wp = Ws[ui][p], wq = Ws[ui][q];
+          Ws[ui][p] = fma(c, wp, -sn * wq);
+          Ws[ui][q] = fma(sn, wp, c * wq);
           __syncthreads();
           cb ^= 1;
         }
