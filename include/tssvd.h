@@ -92,7 +92,11 @@ typedef struct {
   double working_precision;  /* wp in (0,1), default 1e-11 ("could be 10^-11") */
   int orthonormalizations;   /* tssvd: 1 = Algorithm 3, 2 = Algorithm 4 */
   int max_jacobi_sweeps;     /* cap per small core, e.g. 60; exceeded -> TSSVD_ENOCONV */
-  int host_io;               /* 0: device pointers; 1: host pointers (see conventions) */
+  int host_io;               /* 0: device pointers; 1: host pointers (see conventions);
+                                2 (lowrank_svd only): host pointers and A is never resident --
+                                every pass over A streams row chunks of ~256 MB through two
+                                device staging buffers on a library-owned copy stream
+                                (out-of-core; PCIe-bound; workspace without the m x n copy) */
 } tssvd_opts;
 
 /* Fills defaults: wp 1e-11, Algorithm 4, 60 sweeps, device pointers. */

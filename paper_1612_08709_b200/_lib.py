@@ -126,13 +126,13 @@ def check(status: int) -> None:
         raise TssvdError(status, lib().tssvd_last_error().decode())
 
 
-def default_opts(wp: float = 1e-11, passes: int = 2, max_sweeps: int = 60, host_io: bool = False):
+def default_opts(wp: float = 1e-11, passes: int = 2, max_sweeps: int = 60, host_io: int | bool = False):
     o = TssvdOpts()
     lib().tssvd_opts_default(ctypes.byref(o))
     o.working_precision = wp
     o.orthonormalizations = passes
     o.max_jacobi_sweeps = max_sweeps
-    o.host_io = 1 if host_io else 0
+    o.host_io = int(host_io)  # 0 device, 1 host (staged), 2 host (streamed, lowrank_svd)
     return o
 
 

@@ -137,10 +137,13 @@ def tssvd(A: torch.Tensor, wp: float = 1e-11, passes: int = 2, comm: Comm | None
 
 
 def lowrank_svd(A: torch.Tensor, Omega: torch.Tensor, iters: int, k: int | None = None,
-                wp: float = 1e-11, comm: Comm | None = None, max_sweeps: int = 60):
+                wp: float = 1e-11, comm: Comm | None = None, max_sweeps: int = 60,
+                out_of_core: bool = False):
     """Rank-k approximation U diag(sigma) V^T of the row-sharded A by Algorithm 8.
 
     Omega (n x l) is the Gaussian start block of Alg. 5 step 1 (identical on every rank).
+    out_of_core (CPU tensors only): A stays in host memory and every pass over it streams row
+    chunks (opts.host_io = 2) -- for A larger than the GPU's memory.
     """
     _check_tall(A)
     m, n = A.shape
@@ -151,7 +154,9 @@ def lowrank_svd(A: torch.Tensor, Omega: torch.Tensor, iters: int, k: int | None 
         torch.device("cuda", torch.cuda.current_device()) if host else A.device)
     if Omega.device != A.device or Omega.dtype != torch.float64 or Omega.stride(1) != 1:
         raise ValueError("Omega must be float64 on A's device with unit column stride")
-    opts = default_opts(wp, 2, max_sweeps, host_io=host)
+    if out_of_core and not host:
+        raise ValueError("out_of_core needs A in host memory")
+    opts = default_opts(wp, 2, max_sweeps, host_io=2 if out_of_core else host)
     cptr = comm.ptr if comm else None
     nbytes = ctypes.c_size_t()
     check(lib().lowrank_workspace_size(cptr, m, n, l, ctypes.byref(opts), ctypes.byref(nbytes)))

@@ -214,6 +214,13 @@ struct Pass {
 inline int mrows_for(int k) { return (int)(gemm_nn_m_doubles(k, 1) / smem_ld(1)); }
 inline int64_t even(int64_t x) { return (x + 1) & ~int64_t(1); }
 
+int64_t ooc_chunk_rows(int n) {  // ~256 MB per staging buffer (TSSVD_OOC_CHUNK_ROWS overrides)
+  static const int64_t force = getenv("TSSVD_OOC_CHUNK_ROWS") ? atoll(getenv("TSSVD_OOC_CHUNK_ROWS")) : 0;
+  if (force > 0) return force;
+  return std::max<int64_t>(256, (int64_t)(256.0 * (1 << 20) / (8.0 * std::max(n, 1))));
+}
+
+
 // ---------------------------------------------------------------- core ----
 // Buffers of one Alg. 3/4 run on an (m_local x w) matrix.
 struct Core {
@@ -798,7 +805,7 @@ void check_opts(const tssvd_opts* o) {
   if (!(o->working_precision > 0.0 && o->working_precision < 1.0))
     fail(TSSVD_EINVAL, "working precision %g not in (0,1)", o->working_precision);
   if (o->max_jacobi_sweeps < 1) fail(TSSVD_EINVAL, "max_jacobi_sweeps < 1");
-  if (o->host_io != 0 && o->host_io != 1) fail(TSSVD_EINVAL, "host_io must be 0 or 1");
+  if (o->host_io < 0 || o->host_io > 2) fail(TSSVD_EINVAL, "host_io must be 0, 1 or 2");
 }
 
 void set_device(tssvd_comm* comm) {
@@ -950,7 +957,7 @@ struct LrPlan {
   Core tall, small;
   int* ctl;
   double *Qt, *Y, *Z, *tn, *Ut, *sig_tmp, *v_scr, *sig_scr, *Mfin, *sk;
-  double *a_stage, *o_stage, *u_stage, *s_stage, *vo_stage;
+  double *a_stage, *a_stage2, *o_stage, *u_stage, *s_stage, *vo_stage;
   int lp, ldzmax;
 };
 
@@ -971,9 +978,16 @@ size_t plan_lowrank(Arena& a, LrPlan& p, int64_t m_local, int n, int l, const ts
   p.sig_scr = a.get<double>(l);
   p.v_scr = a.get<double>((size_t)std::max(n, l) * l);
   p.Mfin = a.get<double>(gemm_nn_m_doubles(l, l));
-  p.sk = a.get<double>(gemm_nn_scratch_doubles(std::max<int64_t>(m_local, 1), n, l));  // alpha stream-K records
+  // alpha stream-K records: sized for any row count (the out-of-core mode runs it on chunks)
+  p.sk = a.get<double>(gemm_nn_scratch_max(n, l));
+  p.a_stage2 = nullptr;
+  if (o && o->host_io == 2) {  // out-of-core: two chunk-sized staging buffers instead of A
+    const int64_t ch = std::min<int64_t>(std::max<int64_t>(m_local, 1), ooc_chunk_rows(n));
+    p.a_stage = a.get<double>((size_t)ch * even(n));
+    p.a_stage2 = a.get<double>((size_t)ch * even(n));
+  }
   if (o && o->host_io) {
-    p.a_stage = a.get<double>((size_t)std::max<int64_t>(m_local, 1) * even(n));
+    if (o->host_io == 1) p.a_stage = a.get<double>((size_t)std::max<int64_t>(m_local, 1) * even(n));
     p.o_stage = a.get<double>((size_t)n * even(l));
     p.u_stage = a.get<double>((size_t)std::max<int64_t>(m_local, 1) * even(l));  // k <= l columns
     p.s_stage = a.get<double>(l);
@@ -982,18 +996,66 @@ size_t plan_lowrank(Arena& a, LrPlan& p, int64_t m_local, int n, int l, const ts
   return a.off;
 }
 
+// ---- the tall matrix as a source of row chunks (out-of-core mode, host_io = 2) ----
+// In-core, an A-pass is one launch over the resident A.  Streamed, A stays in (pinned) host
+// memory and every A-pass walks it in row chunks: a library-owned copy stream moves chunk
+// c + 1 into one of two device staging buffers while the call's stream runs the pass's kernel
+// on chunk c (events order the reuse).  Row-local passes (alpha: Y = A Q~) write their rows of
+// Y; the reduction over rows (beta: A^T Q) accumulates the chunks' fixed-order partial sums in
+// chunk order, so the result is deterministic.  PCIe-bound by design: it is for A larger than
+// the GPU's memory.
+struct ASource {
+  bool streamed = false;
+  const double* dev = nullptr;  // in-core A (device)
+  int64_t ld = 0;
+  const double* host = nullptr;  // streamed A (host)
+  int64_t hld = 0;
+  int64_t m = 0;
+  int n = 0;
+  int64_t chunk = 0;             // rows per chunk
+  double* stage[2] = {nullptr, nullptr};
+  int64_t sld = 0;               // staging leading dimension (even)
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ready[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr};
+  // f(const double* A_chunk, int64_t ld, int64_t row0, int64_t rows, bool first)
+  template <class F>
+  void each(Ctx& c, F&& f) {
+    if (!streamed) {
+      f(dev, ld, 0, m, true);
+      return;
+    }
+    const int64_t nch = m > 0 ? ceil_div(m, chunk) : 0;
+    for (int64_t q = 0; q < nch; ++q) {
+      const int b = (int)(q & 1);
+      const int64_t r0 = q * chunk, rows = std::min(chunk, m - r0);
+      if (!g_dry) {
+        if (q >= 2) CU(cudaStreamWaitEvent(cs, freed[b], 0));
+        CU(cudaMemcpy2DAsync(stage[b], sld * 8, host + r0 * hld, hld * 8, (size_t)n * 8, rows,
+                             cudaMemcpyHostToDevice, cs));
+        CU(cudaEventRecord(ready[b], cs));
+        CU(cudaStreamWaitEvent(c.s, ready[b], 0));
+      }
+      f(stage[b], sld, r0, rows, q == 0);
+      if (!g_dry) CU(cudaEventRecord(freed[b], c.s));
+    }
+  }
+};
+
 // Z (n x ldo) = sum over ranks of A_p^T Q_p  (Alg. 5 step 5 / Alg. 6 step 1); the
 // split-K partials are summed in a fixed order on the device (36 MB per c3 pass
 // through L2/HBM, ~15 us), then allreduced WITHOUT the partials' pad columns
 // (ldo = r rounded up to even).
-int tn_pass(Ctx& c, LrPlan& p, const double* A, int64_t lda, int64_t m_local, int n, int r) {
+int tn_pass(Ctx& c, LrPlan& p, ASource& src, int64_t m_local, int n, int r) {
   step("beta:%d", r);
-  const TnPlan tp = plan_gemm_tn(std::max<int64_t>(m_local, 1), n, r);
   const int ldo = (r + 1) & ~1;
   if (m_local > 0) {
     Pass t(c.s, TSSVD_PASS_BETA, 2.0 * m_local * n * r, 8.0 * m_local * (n + r));
-    KL(launch_gemm_tn(tp, A, lda, m_local, n, p.Y, p.lp, r, p.tn, c.s));
-    KL(launch_reduce_parts_2d(p.tn, tp.splits, (int64_t)tp.colblocks * tp.cb * tp.ldz, n, tp.ldz, r, p.Z, ldo, true, c.s));
+    src.each(c, [&](const double* A, int64_t lda, int64_t r0, int64_t rows, bool first) {
+      const TnPlan tp = plan_gemm_tn(rows, n, r);
+      KL(launch_gemm_tn(tp, A, lda, rows, n, p.Y + r0 * p.lp, p.lp, r, p.tn, c.s));
+      KL(launch_reduce_parts_2d(p.tn, tp.splits, (int64_t)tp.colblocks * tp.cb * tp.ldz, n, tp.ldz, r, p.Z, ldo,
+                                true, c.s, !first));
+    });
   } else {
     KS(fill(p.Z, (int64_t)n * ldo, 0.0, c.s));
   }
@@ -1017,7 +1079,8 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
   if (k < 1 || k > l) fail(TSSVD_EINVAL, "need 0 < k <= l");
   if (ldo < l || ldu < k || ldv < k) fail(TSSVD_EINVAL, "ldo < l, ldu < k or ldv < k");
   if (!rank) fail(TSSVD_EINVAL, "rank is NULL");
-  const bool hio = opts->host_io == 1;
+  const bool hio = opts->host_io >= 1;
+  const bool streamed = opts->host_io == 2;  // out-of-core: A is never resident
   if (!hio && m_local > 0 && !aligned16(A)) fail(TSSVD_EINVAL, "A must be 16-byte aligned");
   if (!hio && m_local > 0 && (!aligned16(U) || (ldu & 1)))
     fail(TSSVD_EINVAL, "U must be 16-byte aligned with an even ldu");
@@ -1075,47 +1138,74 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
   int64_t ldad = lda;
   const double* Od = Omega;
   int64_t ldod = ldo;
+  ASource src;
+  src.m = m_local;
+  src.n = N;
   if (hio) {
-    step("h2d:A");
-    if (m_local > 0)
-      CUR(cudaMemcpy2DAsync(p.a_stage, even(n) * 8, A, lda * 8, n * 8, m_local, cudaMemcpyHostToDevice, c.s));
+    if (!streamed) {
+      step("h2d:A");
+      if (m_local > 0)
+        CUR(cudaMemcpy2DAsync(p.a_stage, even(n) * 8, A, lda * 8, n * 8, m_local, cudaMemcpyHostToDevice, c.s));
+      Ad = p.a_stage;
+      ldad = even(n);
+    }
     CUR(cudaMemcpy2DAsync(p.o_stage, even(l) * 8, Omega, ldo * 8, l * 8, n, cudaMemcpyHostToDevice, c.s));
-    Ad = p.a_stage;
-    ldad = even(n);
     Od = p.o_stage;
     ldod = even(l);
   }
+  src.dev = Ad;
+  src.ld = ldad;
+  if (streamed) {
+    step("stream:A");
+    src.streamed = true;
+    src.host = A;
+    src.hld = lda;
+    src.chunk = ooc_chunk_rows(N);
+    src.sld = even(n);
+    src.stage[0] = p.a_stage;
+    src.stage[1] = p.a_stage2;
+    if (!g_dry) {
+      static thread_local cudaStream_t cs = nullptr;
+      static thread_local cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+      if (!cs) {
+        CU(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        for (auto& e : ev) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      }
+      src.cs = cs;
+      src.ready[0] = ev[0], src.ready[1] = ev[1], src.freed[0] = ev[2], src.freed[1] = ev[3];
+      CU(cudaEventRecord(ev[2], c.s));  // the copy stream starts after everything before the call
+      CU(cudaStreamWaitEvent(cs, ev[2], 0));
+    }
+  }
+  auto alpha = [&]() {
+    step("alpha:%d", Lc);
+    Pass t(c.s, TSSVD_PASS_ALPHA, 2.0 * m_local * N * Lc, 8.0 * m_local * (N + Lc));
+    src.each(c, [&](const double* Ac, int64_t ldc, int64_t r0, int64_t rows, bool) {
+      KL(launch_gemm_nn(Ac, ldc, rows, N, p.Qt, Lc, p.Y + r0 * p.lp, p.lp, nullptr, p.sk, c.s));
+    });
+    ++g_stats.a_passes;
+  };
   // Every decision stays on the device (no host round trip until the end): the
   // launches are sized by the block width l, and columns past a kept rank are zeros.
   // Alg. 5 step 1: Q~_0 = Omega.
   KS(rows_to_m(Od, ldod, N, Lc, p.Qt, smem_ld(Lc), mrows_for(N), c.s));
   for (int it = 0; it < iters; ++it) {
     // step 3: Y_j = A Q~_{j-1}
-    step("alpha:%d", Lc);
-    {
-      Pass t(c.s, TSSVD_PASS_ALPHA, 2.0 * m_local * N * Lc, 8.0 * m_local * (N + Lc));
-      KL(launch_gemm_nn(Ad, ldad, m_local, N, p.Qt, Lc, p.Y, p.lp, nullptr, p.sk, c.s));
-    }
-    ++g_stats.a_passes;
+    alpha();
     // step 4: Y_j = Q_j R_j by Alg. 3 (Q_j = U, in place in Y)
     core(c, p.tall, p.Y, p.lp, m_local, Lc, 1, true, p.Y, p.lp, p.sig_scr, p.v_scr, Lc, true);
     // step 5: Y~_j = A^* Q_j
-    const int ldz = tn_pass(c, p, Ad, ldad, m_local, N, Lc);
+    const int ldz = tn_pass(c, p, src, m_local, N, Lc);
     // step 6: Y~_j = Q~_j R~_j by Alg. 3 on the replicated n x l matrix
     core(c, p.small, p.Z, ldz, N, Lc, 1, false, p.Z, ldz, p.sig_scr, p.v_scr, Lc, true);
     step("qt");
     KS(rows_to_m(p.Z, ldz, N, Lc, p.Qt, smem_ld(Lc), mrows_for(N), c.s));
   }
   // step 8: Y = A Q~_i; step 9: Y = Q R by Alg. 4
-  step("alpha:%d", Lc);
-  {
-    Pass t(c.s, TSSVD_PASS_ALPHA, 2.0 * m_local * N * Lc, 8.0 * m_local * (N + Lc));
-    KL(launch_gemm_nn(Ad, ldad, m_local, N, p.Qt, Lc, p.Y, p.lp, nullptr, p.sk, c.s));
-  }
-  ++g_stats.a_passes;
+  alpha();
   const CoreOut o3 = core(c, p.tall, p.Y, p.lp, m_local, Lc, 2, true, p.Y, p.lp, p.sig_scr, p.v_scr, Lc, true);
   // Alg. 6 step 1: B^T = A^* Q
-  const int ldz = tn_pass(c, p, Ad, ldad, m_local, N, o3.bound);
+  const int ldz = tn_pass(c, p, src, m_local, N, o3.bound);
   // Alg. 6 step 2: B^T = V Sigma U~^* by Alg. 4 (reading R6); V in place in Z
   const CoreOut o4 = core(c, p.small, p.Z, ldz, N, o3.bound, 2, false, p.Z, ldz, p.sig_tmp, p.Ut, Lc, true);
   step("canon");

@@ -37,6 +37,7 @@ cudaError_t launch_gemm_nn(const double* X, int64_t ldx, int64_t m, int k, const
                            cudaStream_t s);
 size_t gemm_nn_m_doubles(int k, int c);  // size of the padded M buffer
 size_t gemm_nn_scratch_doubles(int64_t m, int k, int c);
+size_t gemm_nn_scratch_max(int k, int c);  // stream-K records for any m (0 if K has one chunk)
 
 // Z (n x l, ld ldz) partials: Zp[split][n_pad x ldz] = X[rows, :n]^T * Y[rows, :l]
 // reduced over `splits` row ranges.
@@ -54,7 +55,8 @@ cudaError_t launch_reduce_parts(const double* part, int nparts, int64_t stride, 
 // out[row*ldo + col] = sum_p part[p*stride + row*ldi + col], col < cols (zeros up to ldo
 // when zero_pad)
 cudaError_t launch_reduce_parts_2d(const double* part, int nparts, int64_t stride, int64_t rows,
-                                   int ldi, int cols, double* out, int ldo, bool zero_pad, cudaStream_t s);
+                                   int ldi, int cols, double* out, int ldo, bool zero_pad, cudaStream_t s,
+                                   bool accumulate = false);  // accumulate: out += the sum
 
 // ---- one-sided Jacobi (jacobi.cu) ----
 // EIG: B (n x n, ldb, symmetric PSD) -> k <= n eigenpairs: vals[j] descending,

@@ -391,7 +391,7 @@ cudaError_t launch_reduce_parts(const double* part, int np, int64_t stride, int6
 // allreduce then moves n x ldo doubles, ldo = l rounded up to even, not n x pad8(l)).
 __global__ void reduce_parts_2d_kernel(const double* __restrict__ part, int np, int64_t stride,
                                        int64_t rows, int ldi, int cols, double* __restrict__ out,
-                                       int ldo, int zero_pad) {
+                                       int ldo, int zero_pad, int accumulate) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= rows * ldo) return;
   const int64_t row = e / ldo;
@@ -410,14 +410,15 @@ __global__ void reduce_parts_2d_kernel(const double* __restrict__ part, int np, 
     for (int q = p0; q < p1; ++q) sum += p[(size_t)q * stride];
     tot += sum;
   }
-  out[e] = tot;
+  out[e] = accumulate ? out[e] + tot : tot;
 }
 
 cudaError_t launch_reduce_parts_2d(const double* part, int np, int64_t stride, int64_t rows, int ldi,
-                                   int cols, double* out, int ldo, bool zero_pad, cudaStream_t s) {
+                                   int cols, double* out, int ldo, bool zero_pad, cudaStream_t s,
+                                   bool accumulate) {
   if (rows <= 0) return cudaSuccess;
   reduce_parts_2d_kernel<<<(int)ceil_div(rows * ldo, 256), 256, 0, s>>>(part, np, stride, rows, ldi,
-                                                                         cols, out, ldo, zero_pad);
+                                                                         cols, out, ldo, zero_pad, accumulate);
   return cudaGetLastError();
 }
 
@@ -826,6 +827,11 @@ int gemm_nn_part_stride(int c) {
   return (sh.niw + (sh.xr > 0)) * sh.wc * 8;
 }
 size_t gemm_nn_m_doubles(int k, int c) { return (size_t)ceil_div(k + 1, 32) * 32 * smem_ld(c); }
+size_t gemm_nn_scratch_max(int k, int c) {  // for any m: the records do not depend on m
+  if (c <= 0 || c > 256) return 0;
+  NnPlan p = plan_nn(1 << 20, std::max(k, 1), c);
+  return p.kcc >= 2 ? (size_t)2 * dev_info().sms * p.R * p.cp : 0;
+}
 size_t gemm_nn_scratch_doubles(int64_t m, int k, int c) {
   if (c <= 0 || c > 256) return 0;
   const NnPlan p = plan_nn(std::max<int64_t>(m, 1), std::max(k, 1), c);

@@ -650,3 +650,19 @@ def test_tssvd_paper_staircase_table21_gpu(passes, key):
     # orthonormality ~5e-15; ours ~1e-13 orthonormality gives ~2e-13): a factor 20 either way
     assert g["spectral_error"] / 20 <= err <= 20 * g["spectral_error"]
     assert info["ortho_v"] <= 1e-13
+
+
+def test_lowrank_out_of_core_matches_in_core():
+    """opts.host_io = 2: A never resident, every alpha/beta pass streams row
+    chunks (n = 4000: ~8192 rows per chunk, so m = 20,000 is three chunks with the copy of one
+    overlapping the pass over the other).  Row-local alpha results are bit-identical to the
+    in-core run; beta's chunk-ordered partial sums differ only by rounding: the parity contract
+    against the oracle holds."""
+    d = synth.config_inputs("c3", m=20_000, n=4_000)
+    a, om = torch.from_numpy(d["A"]).pin_memory(), torch.from_numpy(d["Omega"]).pin_memory()
+    uo, so, vo = tk.lowrank_svd(a, om, d["iters"], d["k"], out_of_core=True)
+    gpu = (uo.numpy(), so.numpy(), vo.numpy())
+    ref = oracle.lowrank_svd(d["A"], d["Omega"], d["iters"], d["k"])
+    print(assert_lowrank_parity(gpu, ref, d["A"], d["x0"]))
+    ud, sd, vd = lowrank_gpu(d["A"], d["Omega"], d["iters"], d["k"])
+    assert np.max(np.abs(so.numpy() - sd)) <= 1e-13 * sd[0]
