@@ -181,15 +181,23 @@ struct PassTimer {
     g_stats.pass_kind[i] = kind;
     g_stats.pass_flops[i] = flops;
     g_stats.pass_bytes[i] = bytes;
-    CU(cudaEventRecord(ev[2 * i], st));
+    CU(record(ev[2 * i], st));
     open = i;
     s = st;
   }
   void end() {
     if (open < 0) return;
-    cudaEventRecord(ev[2 * open + 1], s);  // no throw: runs in a destructor
+    record(ev[2 * open + 1], s);  // no throw: runs in a destructor
     g_stats.n_pass = open + 1;
     open = -1;
+  }
+  // Inside a stream capture a plain cudaEventRecord only orders the capture; the graph gets
+  // an event-record node (so the timing events fire on every replay) with the External flag.
+  static cudaError_t record(cudaEvent_t e, cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive)
+      return cudaEventRecordWithFlags(e, st, cudaEventRecordExternal);
+    return cudaEventRecord(e, st);
   }
   void create_all() {  // before a graph capture: no event creation inside it
     for (auto& e : ev)

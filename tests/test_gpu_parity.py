@@ -666,3 +666,20 @@ def test_lowrank_out_of_core_matches_in_core():
     print(assert_lowrank_parity(gpu, ref, d["A"], d["x0"]))
     ud, sd, vd = lowrank_gpu(d["A"], d["Omega"], d["iters"], d["k"])
     assert np.max(np.abs(so.numpy() - sd)) <= 1e-13 * sd[0]
+
+
+def test_pass_timing_with_graph_replay():
+    """Per-pass CUDA-event timing (bench.py's roofline) through a captured-and-replayed call:
+    the events must be graph event-record nodes (a plain record inside a capture is not)."""
+    from paper_1612_08709_b200 import _lib
+
+    d = synth.config_inputs("c3", m=4_000, n=1_000)
+    A, om = to_dev(d["A"]), to_dev(d["Omega"])
+    _lib.set_pass_timing(True)
+    try:
+        for _ in range(3):  # capture, then replays
+            tk.lowrank_svd(A, om, d["iters"], d["k"])
+            passes = _lib.last_stats()["passes"]
+            assert passes and all(p["ms"] > 0 for p in passes)
+    finally:
+        _lib.set_pass_timing(False)
