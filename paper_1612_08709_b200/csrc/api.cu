@@ -1033,6 +1033,12 @@ struct ASource {
       return;
     }
     const int64_t nch = m > 0 ? ceil_div(m, chunk) : 0;
+    // the staging buffers are free once the stream's earlier work is done (the previous pass
+    // may still be reading them): the pass's first copies wait for it
+    if (!g_dry && nch > 0) {
+      CU(cudaEventRecord(freed[0], c.s));
+      CU(cudaStreamWaitEvent(cs, freed[0], 0));
+    }
     for (int64_t q = 0; q < nch; ++q) {
       const int b = (int)(q & 1);
       const int64_t r0 = q * chunk, rows = std::min(chunk, m - r0);
@@ -1181,8 +1187,6 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
       }
       src.cs = cs;
       src.ready[0] = ev[0], src.ready[1] = ev[1], src.freed[0] = ev[2], src.freed[1] = ev[3];
-      CU(cudaEventRecord(ev[2], c.s));  // the copy stream starts after everything before the call
-      CU(cudaStreamWaitEvent(cs, ev[2], 0));
     }
   }
   auto alpha = [&]() {
