@@ -598,7 +598,13 @@ CoreOut core(Ctx& c, Core& b, const double* X, int64_t ldx, int64_t m_local, int
 //     still alias A (A is not read after the A V~ pass);
 //   * the eigensolver / SVD of width > 256: the cooperative solvers of jacobi_wide.cu;
 //   * host decisions for k and r (the panels are sized by them), r' on the device.
-constexpr int kWideMax = 2048, kPanel = 256, kGramPanel = 128;
+constexpr int kWideMax = 2048, kGramPanel = 128;
+// column-panel width of the wide products (TSSVD_WIDE_PANEL overrides, experiments)
+int wide_panel() {
+  static const int v = getenv("TSSVD_WIDE_PANEL") ? atoi(getenv("TSSVD_WIDE_PANEL")) : 256;
+  return std::max(8, std::min(256, v));
+}
+constexpr int kPanel = 256;  // buffer bound
 
 struct WideCore {
   int w = 0;
@@ -669,8 +675,9 @@ void wide_product(Ctx& c, WideCore& b, const double* X, int64_t ldx, int64_t m_l
                   int ldm, int cols, double* Y, int64_t ldy, double* nsq_out, int pass_kind) {
   cudaStream_t s = c.s;
   Pass t(s, pass_kind, 2.0 * m_local * k * cols, 8.0 * m_local * (k + cols));
-  for (int c0 = 0; c0 < cols; c0 += kPanel) {
-    const int cw = std::min(kPanel, cols - c0);
+  const int pw = wide_panel();
+  for (int c0 = 0; c0 < cols; c0 += pw) {
+    const int cw = std::min(pw, cols - c0);
     KS(rows_to_m(M + c0, ldm, k, cw, b.Mp, smem_ld(cw), mrows_for(k), s));
     KL(launch_gemm_nn(X, ldx, m_local, k, b.Mp, cw, Y ? Y + c0 : nullptr, ldy, nsq_out ? b.npart : nullptr,
                       nullptr, s));
