@@ -5,6 +5,17 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+// Device-side bounds checks, compiled in only for the checking build
+// (`python paper_1612_08709_b200/build.py --out tools/ab/libtssvd_checks.so -D TSSVD_CHECKS`,
+// loaded through TSSVD_LIB): compute-sanitizer is closed on this pool, so the GPU test suite
+// runs against this build instead -- a failed check traps the kernel and fails the test.
+#ifdef TSSVD_CHECKS
+#include <cassert>
+#define TCHECK(c) assert(c)
+#else
+#define TCHECK(c) ((void)0)
+#endif
+
 namespace tsk {
 
 constexpr double kEps = 2.220446049250313e-16;

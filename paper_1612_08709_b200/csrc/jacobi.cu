@@ -227,6 +227,7 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
   }
   const int nslots = a.mode == 0 ? a.n : a.N;
   const int P = a.P, Lh = a.Lh;
+  TCHECK(nslots <= JMAX && Lh <= P && a.V * 2 * (P / (2 * a.V)) == P);
   const int row0 = h * Lh;                         // first global row held here
   const int nloc = max(0, min(Lh, a.L - row0));    // rows held here
   double* X = dsm;                                 // [nslots][P]
@@ -656,6 +657,7 @@ __global__ void __launch_bounds__(JT, 1) jacobi_kernel(const JacArgs a) {
       double2* xp = nullptr;
       double2* xq = nullptr;
       if (has) {
+        TCHECK(pos_p < NE && pos_q < NE && s_order[pos_p] <= nslots && s_order[pos_q] <= nslots);
         xp = reinterpret_cast<double2*>(X + s_order[pos_p] * P) + gl;
         xq = reinterpret_cast<double2*>(X + s_order[pos_q] * P) + gl;
 #pragma unroll

@@ -159,6 +159,7 @@ __global__ void __launch_bounds__(WT, 1) wide_pchol_kernel(const PcholArgs a) {
       tabs = a.trunc * dp;
     }
     if (nonfinite || p < 0 || !(dp > tabs)) break;
+    TCHECK(p < n && k < n && G <= 256);
     // stage row p of X (columns < k), written by its owner before the barrier
     for (int j = tid; j < k; j += WT) xp[j] = __ldcg(a.X + (size_t)p * n + j);
     __syncthreads();
@@ -308,6 +309,7 @@ __global__ void __launch_bounds__(WT, 1) wide_bjacobi_kernel(const BjArgs a) {
 #pragma unroll
           for (int q = 0; q < WPER; ++q) cur[q] = nxt[q];
         }
+        TCHECK(u < 256 && bp < nb && bq < nb && bp != bq);
         double* gp = a.gpart + (size_t)u * WPC * WPC;
         gp[(ti * 8 + g) * WPC + tj * 8 + 2 * t] = acc[0];
         gp[(ti * 8 + g) * WPC + tj * 8 + 2 * t + 1] = acc[1];

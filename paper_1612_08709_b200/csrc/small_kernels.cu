@@ -111,6 +111,7 @@ __global__ void k_alg3_out(const double* sig, const int* idx, const int* rr, int
     return;
   }
   const int ja = idx[a];
+  TCHECK(ja >= 0 && ja < w && r <= rb && rb <= ldm);
   const double sa = sig[ja];
   int rk = 0;
   for (int b = 0; b < r; ++b) {
@@ -184,6 +185,7 @@ __global__ void __launch_bounds__(256) k_svd_out(const double* cols, int ldc, co
   __shared__ int sbi[8][SVO_COLS];
   __shared__ double ssign[SVO_COLS];
   const int r2 = *rr2, r = *rr;
+  TCHECK(r <= 256 && r2 <= rb2 && w <= 256);  // sJ / sidx rows, one thread per row of V
   const int a0 = blockIdx.x * SVO_COLS, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nall = min(SVO_COLS, rb2 - a0);           // output columns of this CTA
   const int na = max(0, min(SVO_COLS, r2 - a0));      // ... that are real
@@ -253,6 +255,7 @@ __global__ void __launch_bounds__(256) k_build_m2(const double* W, int ldw, cons
   const int b = blockIdx.x;
   if (b >= *rr) return;
   const int r2 = *rr2;
+  TCHECK(r2 <= 256 && r2 <= ldm);
   for (int c = threadIdx.x; c < r2; c += blockDim.x) {
     const int c2 = idx2[c];
     wrow[c] = W[(size_t)c2 * ldw + b] / T[c2];

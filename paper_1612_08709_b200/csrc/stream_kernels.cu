@@ -212,9 +212,11 @@ __global__ void __launch_bounds__(512, MINB) syrk_kernel(const __grid_constant__
   }
 
   double* P = part + (size_t)rb * wp * wp;
+  TCHECK(rb < (int)gridDim.y && I0 * 8 < wp);
 #pragma unroll
   for (int k = 0; k < TPW; ++k)
     if (k < nt)
+      TCHECK((int)(off[k] >> 16) + g < wp && (int)(off[k] & 0xffffu) + 2 * t + 1 < wp),
       *reinterpret_cast<double2*>(P + (size_t)((off[k] >> 16) + g) * wp + (off[k] & 0xffffu) + 2 * t) =
           make_double2(acc[k][0], acc[k][1]);
 }
@@ -535,6 +537,7 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
     mbar_wait(ring.full(b), (uint32_t)((s / nst) & 1));
     const double* xs = buf + b * stage_d + (rg * MI * 8 + g) * KC + t;
     const double* ms = buf + b * stage_d + xs_d + t * LDM + col0 + g;
+    TCHECK(((rg * MI + MI - 1) * 8 + g) * KC + t + KC - 4 < xs_d && col0 + (NIW - 1) * 8 + g < LDM + 8 * XR);
     int64_t tile = 0;
     int kc_here;
     if constexpr (SK) {
@@ -594,6 +597,7 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
     if (SK && partial && (kc_here == kc_count - 1 || s == nsteps - 1)) {
       // stream-K partial tile: accumulators to this CTA's record (summed by gemm_nn_fixup)
       double* rec = sk_rec + (size_t)(2 * blockIdx.x + (tile == first_tile ? 0 : 1)) * R * CP;
+      TCHECK(tile >= first_tile && tile < ntiles && col0 + NIW * 8 <= CP);
 #pragma unroll
       for (int i = 0; i < MI; ++i) {
         const int row = (rg * MI + i) * 8 + g;
@@ -1014,6 +1018,7 @@ __global__ void __launch_bounds__(32 * (TN_CW + 1)) gemm_tn_kernel(
   }
 
   double* P = part + (size_t)blockIdx.y * n_pad * ldz;
+  TCHECK(c0 + CB <= n_pad && NBL * 8 <= ldz);
 #pragma unroll
   for (int i = 0; i < MI; ++i) {
     const int row = c0 + (warp * MI + i) * 8 + g;
