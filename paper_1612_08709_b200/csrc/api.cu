@@ -601,7 +601,10 @@ CoreOut core(Ctx& c, Core& b, const double* X, int64_t ldx, int64_t m_local, int
 constexpr int kWideMax = 2048, kGramPanel = 128;
 // column-panel width of the wide products (TSSVD_WIDE_PANEL overrides, experiments)
 int wide_panel() {
-  static const int v = getenv("TSSVD_WIDE_PANEL") ? atoi(getenv("TSSVD_WIDE_PANEL")) : 256;
+  // 96: measured on the paper's Table 3 matrix (1e6 x 2000; tools/nn_bench.py + bench t3):
+  // panels of 256 ran the GEMM at 18 TF (one row block per warp), 96-192 at 32-33 TF;
+  // t3 515 -> 400 ms per call
+  static const int v = getenv("TSSVD_WIDE_PANEL") ? atoi(getenv("TSSVD_WIDE_PANEL")) : 96;
   return std::max(8, std::min(256, v));
 }
 constexpr int kPanel = 256;  // buffer bound

@@ -759,7 +759,9 @@ static NnShape nn_shape(int c) {
   // (c4 A V~ 13.36 -> 13.14 ms); below 12 the padded column block costs more
   // (c2, 9 blocks: 1.02 -> 1.09 ms).  TSSVD_NN_WC2 moves the threshold (experiments).
   static const int wc2_from = getenv("TSSVD_NN_WC2") ? atoi(getenv("TSSVD_NN_WC2")) : 12;
-  sh.wc = sh.ni < wc2_from || sh.xr ? 1 : 2;
+  // four column groups from wc4_from column blocks on (experiments: TSSVD_NN_WC4)
+  static const int wc4_from = getenv("TSSVD_NN_WC4") ? atoi(getenv("TSSVD_NN_WC4")) : 99;
+  sh.wc = sh.ni < wc2_from || sh.xr ? 1 : (sh.ni >= wc4_from && sh.ni >= 20 && sh.ni % 4 == 0 ? 4 : 2);
   sh.niw = (sh.ni + sh.wc - 1) / sh.wc;
   sh.mi = std::max(1, std::min(4, 24 / sh.niw));
   // remainder-column shapes (c = 8j + 1/2, j <= 4): TSSVD_NN_MI = 2/3/4 row blocks per warp
@@ -907,6 +909,13 @@ cudaError_t launch_gemm_nn(const double* X, int64_t ldx, int64_t m, int k, const
       default: return cudaErrorInvalidValue;
     }
 #undef NN_WCASE
+#define NN_W4CASE(N) \
+  case N: return nn_ni_go<N, 0, 4>(p, tx, tm, m, k, c, Y, ldy, norm_part, sk_rec, s);
+  if (p.sh.wc == 4) switch (p.ni) {
+      NN_W4CASE(20) NN_W4CASE(24) NN_W4CASE(28) NN_W4CASE(32)
+      default: break;  // other widths: two column groups
+    }
+#undef NN_W4CASE
 #define NN_CASE(N) \
   case N: return nn_ni_go<N>(p, tx, tm, m, k, c, Y, ldy, norm_part, sk_rec, s);
   switch (p.ni) {
