@@ -537,7 +537,7 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
     mbar_wait(ring.full(b), (uint32_t)((s / nst) & 1));
     const double* xs = buf + b * stage_d + (rg * MI * 8 + g) * KC + t;
     const double* ms = buf + b * stage_d + xs_d + t * LDM + col0 + g;
-    TCHECK(((rg * MI + MI - 1) * 8 + g) * KC + t + KC - 4 < xs_d && col0 + (NIW - 1) * 8 + g < LDM + 8 * XR);
+    TCHECK(((rg * MI + MI - 1) * 8 + g) * KC + t + KC - 4 < xs_d && col0 + (NIW - 1) * 8 + g < LDM);
     int64_t tile = 0;
     int kc_here;
     if constexpr (SK) {
@@ -760,8 +760,11 @@ static NnShape nn_shape(int c) {
   // (c2, 9 blocks: 1.02 -> 1.09 ms).  TSSVD_NN_WC2 moves the threshold (experiments).
   static const int wc2_from = getenv("TSSVD_NN_WC2") ? atoi(getenv("TSSVD_NN_WC2")) : 12;
   // four column groups from wc4_from column blocks on (experiments: TSSVD_NN_WC4)
-  static const int wc4_from = getenv("TSSVD_NN_WC4") ? atoi(getenv("TSSVD_NN_WC4")) : 99;
-  sh.wc = sh.ni < wc2_from || sh.xr ? 1 : (sh.ni >= wc4_from && sh.ni >= 20 && sh.ni % 4 == 0 ? 4 : 2);
+  // four column groups from 20 column blocks on (3 x 5..8 tiles per warp instead of 1 x 10..16:
+  // c = 160..256 at 29-33 TF instead of 16-30; measured r2, tools/nn_bench.py); TSSVD_NN_WC4
+  // moves the threshold (experiments)
+  static const int wc4_from = getenv("TSSVD_NN_WC4") ? atoi(getenv("TSSVD_NN_WC4")) : 20;
+  sh.wc = sh.ni < wc2_from || sh.xr ? 1 : (sh.ni >= wc4_from && sh.ni >= 20 ? 4 : 2);
   sh.niw = (sh.ni + sh.wc - 1) / sh.wc;
   sh.mi = std::max(1, std::min(4, 24 / sh.niw));
   // remainder-column shapes (c = 8j + 1/2, j <= 4): TSSVD_NN_MI = 2/3/4 row blocks per warp
@@ -789,7 +792,9 @@ static NnPlan plan_nn(int64_t m, int k, int c) {
   p.ni = p.sh.ni;
   const int ncw = nn_cw(p.sh.mi, p.sh.niw, p.sh.wc);
   p.R = 8 * p.sh.mi * (ncw / p.sh.wc);
-  p.ldm = std::min(smem_ld(c), 256);  // smem row stride of the M box (TMA box limit)
+  // smem row stride of the M box: covers every column block a warp reads (the padded last one
+  // included, zero-filled by TMA beyond M's width), TMA box limit 256
+  p.ldm = std::min(smem_ld(std::max(c, p.sh.niw * p.sh.wc * 8)), 256);
   const size_t red = (size_t)ncw * (p.sh.niw + (p.sh.xr > 0)) * 8 * 8;
   const size_t budget = dev_info().smem_optin - kBarBytes - red;
   double best = 1e300;
@@ -912,8 +917,9 @@ cudaError_t launch_gemm_nn(const double* X, int64_t ldx, int64_t m, int k, const
 #define NN_W4CASE(N) \
   case N: return nn_ni_go<N, 0, 4>(p, tx, tm, m, k, c, Y, ldy, norm_part, sk_rec, s);
   if (p.sh.wc == 4) switch (p.ni) {
-      NN_W4CASE(20) NN_W4CASE(24) NN_W4CASE(28) NN_W4CASE(32)
-      default: break;  // other widths: two column groups
+      NN_W4CASE(20) NN_W4CASE(21) NN_W4CASE(22) NN_W4CASE(23) NN_W4CASE(24) NN_W4CASE(25) NN_W4CASE(26)
+      NN_W4CASE(27) NN_W4CASE(28) NN_W4CASE(29) NN_W4CASE(30) NN_W4CASE(31) NN_W4CASE(32)
+      default: return cudaErrorInvalidValue;
     }
 #undef NN_W4CASE
 #define NN_CASE(N) \
