@@ -1,6 +1,6 @@
 """ORACLE -- test infrastructure, NOT part of the product.
 
-Plain CPU float64 implementation of the paper's Algorithms 3, 4, 5, 6, 8 and of
+Plain CPU float64 implementation of the paper's Algorithms 1-8 and of
 its accuracy measures, written from PAPER.md step by step.  Only ``tests/``,
 ``__graft_entry__.smoke()`` and ``bench.py`` (cpu_baseline / --impl reference)
 may import it.  It shares no code with ``paper_1612_08709_b200``.
@@ -11,6 +11,8 @@ values); none is "parity unpinned".
 """
 from .gram_svd import (  # noqa: F401
     DEFAULT_WP,
+    alg1,
+    alg2,
     alg3,
     alg4,
     canonical_signs,
@@ -19,6 +21,10 @@ from .gram_svd import (  # noqa: F401
     gram,
     keep_mask,
     lowrank_svd,
+    lowrank_svd_tsqr,
+    mix_rows,
+    r_keep,
+    tsqr_svd,
     split_rows,
     subspace_iteration,
     sym_eig,

@@ -257,3 +257,124 @@ def lowrank_svd(a: np.ndarray, omega: np.ndarray, i: int, k: int | None = None,
     kk = min(k, s.size)
     u, v = canonical_signs(u[:, :kk], v[:, :kk])
     return u, s[:kk], v
+
+
+# ------------------------------------------- Algorithms 1, 2, 7 (TSQR) --
+def mix_rows(a: np.ndarray, phases: np.ndarray, perms: np.ndarray, inverse: bool = False) -> np.ndarray:
+    """Remark 'randomness': Omega = D F S D~ F S~ applied to every row of A (every
+    column of A^*), the real rows viewed as h = n // 2 complex numbers (pairs (x_2k, x_2k+1) =
+    real and imaginary parts).  phases = [theta_D (h), theta_D~ (h)] (D = diag(exp(i theta)));
+    perms = [S (h), S~ (h)] with (S z)_k = z_{S[k]}; F = the unitary DFT of length h.  Reading
+    R17: for odd n the last real entry is left unmixed.  inverse=True applies Omega^{-1} = Omega^*.
+    """
+    a = np.asarray(a, dtype=np.float64)
+    n = a.shape[1]
+    h = n // 2
+    out = a.copy()
+    z = a[:, 0:2 * h:2] + 1j * a[:, 1:2 * h:2]
+    d1, d2 = np.exp(1j * phases[:h]), np.exp(1j * phases[h:2 * h])
+    s1, s2 = perms[:h].astype(np.int64), perms[h:2 * h].astype(np.int64)
+    if not inverse:  # z <- D F S D~ F S~ z  (rightmost first)
+        z = z[:, s2]
+        z = np.fft.fft(z, axis=1, norm="ortho")
+        z = z * d2[None, :]
+        z = z[:, s1]
+        z = np.fft.fft(z, axis=1, norm="ortho")
+        z = z * d1[None, :]
+    else:  # z <- S~^-1 F^* D~^* S^-1 F^* D^* z
+        z = z * np.conj(d1)[None, :]
+        z = np.fft.ifft(z, axis=1, norm="ortho")
+        w = np.empty_like(z)
+        w[:, s1] = z
+        z = w * np.conj(d2)[None, :]
+        z = np.fft.ifft(z, axis=1, norm="ortho")
+        w = np.empty_like(z)
+        w[:, s2] = z
+        z = w
+    out[:, 0:2 * h:2] = z.real
+    out[:, 1:2 * h:2] = z.imag
+    return out
+
+
+def r_keep(r: np.ndarray, wp: float) -> np.ndarray:
+    """Alg. 1 step 3 / Alg. 2 steps 3, 5: 'view any diagonal
+    entry of R as numerically zero that is less than the first diagonal entry of R times the
+    working precision' (magnitudes: R's diagonal signs are a convention of the QR)."""
+    d = np.abs(np.diag(r))
+    if d.size == 0 or d[0] == 0.0:
+        return np.zeros(d.shape, dtype=bool)
+    return d >= d[0] * wp
+
+
+def alg1(a: np.ndarray, phases: np.ndarray, perms: np.ndarray, wp: float = DEFAULT_WP):
+    """Algorithm 1: randomized TSQR-based SVD of a tall-skinny matrix.
+    'Using the TSQR method compute B^* = Q R' is a QR factorization (TSQR is how the paper
+    distributes it; the factorization is unique up to the signs of R's rows): LAPACK's
+    Householder QR here.  Returns U (m x r), sigma (r, descending), V (n x r)."""
+    _check(a, wp)
+    # Step 1 (P:527-529): B = Omega A^*, i.e. B^* = A Omega^* = every row of A mixed.
+    bs = mix_rows(a, phases, perms)
+    # Step 2 (P:531-532): B^* = Q R.
+    q, r = np.linalg.qr(bs, mode="reduced")
+    # Step 3 (P:534-538): discard rows of R with numerically zero diagonal, columns of Q.
+    keep = r_keep(r, wp)
+    q, r = q[:, keep], r[keep, :]
+    # Step 4 (P:540-543): R = U~ Sigma V~^*.
+    ut, sig, vth = np.linalg.svd(r, full_matrices=False)
+    # Step 5 (P:545): U = Q U~.  Step 6 (P:547-549): V = Omega^{-1} V~.
+    u = q @ ut
+    v = mix_rows(vth, phases, perms, inverse=True).T
+    return u, sig, v
+
+
+def alg2(a: np.ndarray, phases: np.ndarray, perms: np.ndarray, wp: float = DEFAULT_WP):
+    """Algorithm 2: Algorithm 1 with double orthonormalization."""
+    _check(a, wp)
+    # Step 1 (P:567-569): B^* = every row of A mixed.
+    bs = mix_rows(a, phases, perms)
+    # Step 2 (P:571-573): B^* = Q~ R~.  Step 3 (P:575-579): discard.
+    qt, rt = np.linalg.qr(bs, mode="reduced")
+    keep = r_keep(rt, wp)
+    qt, rt = qt[:, keep], rt[keep, :]
+    # Step 4 (P:581-583): Q~ = Q R.  Step 5 (P:585-589): discard.
+    q, r = np.linalg.qr(qt, mode="reduced")
+    keep2 = r_keep(r, wp)
+    q, r = q[:, keep2], r[keep2, :]
+    # Step 6 (P:591): T = R R~.  Step 7 (P:593-596): T = U~ Sigma V~^*.
+    t = r @ rt
+    ut, sig, vth = np.linalg.svd(t, full_matrices=False)
+    # Step 8 (P:598): U = Q U~.  Step 9 (P:600-602): V = Omega^{-1} V~.
+    u = q @ ut
+    v = mix_rows(vth, phases, perms, inverse=True).T
+    return u, sig, v
+
+
+def tsqr_svd(a: np.ndarray, phases: np.ndarray, perms: np.ndarray, wp: float = DEFAULT_WP, passes: int = 2):
+    """Problem {1} by Alg. 2 (passes=2) or Alg. 1 (passes=1), canonical signs (R5)."""
+    u, s, v = (alg2 if passes == 2 else alg1)(a, phases, perms, wp)
+    return canonical_signs(u, v)[0], s, canonical_signs(u, v)[1]
+
+
+def lowrank_svd_tsqr(a: np.ndarray, omega: np.ndarray, i: int, k: int | None, mixes,
+                     wp: float = DEFAULT_WP):
+    """Algorithm 7 = Alg. 6 fed with Alg. 5 using Alg. 1 (steps 4, 6) and Alg. 2
+    (the last step); reading R6: Alg. 6's SVD of B is Alg. 2 on B^T.  mixes(width) returns the
+    (phases, perms) of the random orthogonal matrix for a width-`width` factorization (each
+    factorization's own Omega; seeded by the caller, shared with the CUDA path)."""
+    m, n = a.shape
+    l = omega.shape[1]
+    k = l if k is None else k
+    qt = omega
+    for _ in range(i):
+        y = a @ qt
+        q, _, _ = alg1(y, *mixes(y.shape[1]), wp)
+        yt = a.T @ q
+        qt, _, _ = alg1(yt, *mixes(yt.shape[1]), wp)
+    y = a @ qt
+    q, _, _ = alg2(y, *mixes(y.shape[1]), wp)
+    bt = a.T @ q
+    v, sig, ut = alg2(bt, *mixes(bt.shape[1]), wp)
+    u = q @ ut
+    kk = min(k, sig.size)
+    u, v = canonical_signs(u[:, :kk], v[:, :kk])
+    return u, sig[:kk], v

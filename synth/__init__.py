@@ -21,6 +21,7 @@ from .matrices import (  # noqa: F401
     devils_staircase,
     paper_staircase_matrix,
     omega,
+    mixing_params,
     power_start,
     config_inputs,
 )

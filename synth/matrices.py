@@ -209,6 +209,25 @@ def paper_staircase_matrix(m: int, n: int, rows: tuple[int, int] | None = None) 
     return a, s
 
 
+def mixing_params(n: int, seed: int, stream: int = 6) -> tuple[np.ndarray, np.ndarray]:
+    """The random numbers of Omega = D F S D~ F S~ (Remark 'randomness') for width n
+    (h = n // 2 complex slots): phases [theta_D (h), theta_D~ (h)] uniform in [0, 2 pi), and
+    permutations [S (h), S~ (h)] of 0..h-1 by the Fisher-Yates-Durstenfeld shuffle (the draws of
+    the method, passed to both paths as inputs)."""
+    h = n // 2
+    g = np.random.Generator(np.random.Philox(key=np.array([seed, stream], dtype=np.uint64),
+                                             counter=np.array([0, n, 0, 0], dtype=np.uint64)))
+    phases = g.uniform(0.0, 2.0 * math.pi, size=2 * h)
+    perms = np.empty(2 * h, dtype=np.int32)
+    for half in range(2):
+        p = np.arange(h, dtype=np.int32)
+        for i in range(h - 1, 0, -1):  # Durstenfeld: swap p[i] with p[j], j uniform in [0, i]
+            j = int(g.integers(0, i + 1))
+            p[i], p[j] = p[j], p[i]
+        perms[half * h:(half + 1) * h] = p
+    return phases, perms
+
+
 def omega(n: int, l: int, seed: int) -> np.ndarray:
     """Alg. 5 step 1: n x l i.i.d. centred Gaussian start block, shared by both paths."""
     return normal_block(seed, STREAM_OMEGA, 0, n, l)

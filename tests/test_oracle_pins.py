@@ -347,3 +347,91 @@ def test_paper_table21_staircase(passes, key):
     assert oracle.ortho_error(u) <= 10 * g["max_UtU_minus_I"]
     assert oracle.ortho_error(v) <= 10 * g["max_VtV_minus_I"]
     assert np.max(np.abs(s - sig[: s.size])) <= 1e-12
+
+
+# ------------------------------------------ Algorithms 1, 2, 7 (TSQR) --
+def test_mixing_closed_forms():
+    """Remark 'randomness': Omega = D F S D~ F S~ on pairs viewed as complex numbers.
+    n = 2 (h = 1: F = 1, S = id): a plane rotation by theta_D + theta_D~; n = 4 (h = 2:
+    F = [[1, 1], [1, -1]] / sqrt 2) written out by hand; any n: orthogonal, norm-preserving, and
+    the inverse map undoes it; odd n leaves the last entry alone (reading R17)."""
+    ph = np.array([0.3, 1.1])
+    om = oracle.mix_rows(np.eye(2), ph, np.array([0, 0]))
+    c, s = np.cos(1.4), np.sin(1.4)
+    assert np.allclose(om, [[c, s], [-s, c]], atol=1e-15)  # row k = Omega e_k
+    ph = np.array([0.2, 0.7, 1.3, 2.9])
+    pm = np.array([1, 0, 0, 1])  # S swaps, S~ = id
+    x = np.array([0.5, -1.0, 2.0, 0.25])
+    z = np.array([x[0] + 1j * x[1], x[2] + 1j * x[3]])
+    f = np.array([[1, 1], [1, -1]]) / np.sqrt(2)
+    z = f @ z                                  # F S~ z (S~ = id)
+    z = np.exp(1j * ph[2:]) * z                # D~
+    z = z[[1, 0]]                              # S
+    z = np.exp(1j * ph[:2]) * (f @ z)          # D F
+    want = np.array([z[0].real, z[0].imag, z[1].real, z[1].imag])
+    assert np.allclose(oracle.mix_rows(x[None, :], ph, pm)[0], want, atol=1e-15)
+    for n in (10, 37, 100):
+        ph, pm = synth.mixing_params(n, 3)
+        om = oracle.mix_rows(np.eye(n), ph, pm)
+        assert np.max(np.abs(om @ om.T - np.eye(n))) <= 1e-14
+        assert np.max(np.abs(oracle.mix_rows(om, ph, pm, inverse=True) - np.eye(n))) <= 1e-14
+        if n % 2:
+            assert om[n - 1, n - 1] == 1.0 and np.all(om[n - 1, :n - 1] == 0.0)
+        for half in range(2):
+            assert sorted(pm[half * (n // 2):(half + 1) * (n // 2)]) == list(range(n // 2))
+
+
+@pytest.mark.parametrize("alg", ["alg1", "alg2"])
+def test_alg12_constructed_and_tiny(alg):
+    """Alg. 1 / 2 on c1's constructed spectrum (sigma, U, V against the true
+    factors: QR-based, so no squaring of the condition number -- sigma to 1e-15 sigma_1) and on
+    random tiny matrices against numpy's SVD of A itself."""
+    f = getattr(oracle, alg)
+    d = synth.config_inputs("c1")
+    ph, pm = synth.mixing_params(10, 1)
+    u, s, v = f(d["A"], ph, pm, 1e-11)
+    assert s.size == 10
+    assert np.max(np.abs(s - d["sigma"])) <= 1e-15 * 4
+    assert oracle.ortho_error(u) <= 1e-14 and oracle.ortho_error(v) <= 1e-14
+    assert np.max(np.abs(d["A"] - (u * s) @ v.T)) <= 1e-15 * 10
+    rng = np.random.default_rng(7)
+    for trial in range(20):
+        m, n = int(rng.integers(5, 60)), int(rng.integers(1, 5)) * 2
+        m = max(m, n)
+        a = rng.standard_normal((m, n))
+        ph, pm = synth.mixing_params(n, trial)
+        u, s, v = f(a, ph, pm, 1e-11)
+        ref = np.linalg.svd(a, compute_uv=False)
+        assert np.allclose(s, ref, rtol=1e-12, atol=1e-13 * ref[0])
+        assert np.max(np.abs(a - (u * s) @ v.T)) <= 1e-13 * ref[0]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("alg,key", [("alg1", "alg1_m1e4_n2000"), ("alg2", "alg2_m1e4_n2000")])
+def test_paper_table5_alg12(alg, key):
+    """PAPER.md:970-971 (Table 5, Algorithms 1 and 2, m = 1e4, n = 2000): residual 9.76e-12.  The
+    kept rank follows R's diagonal against R_11 wp, which depends on the random Omega, so the
+    residual (~ the first dropped sigma, ~1e-11) is pinned to 10%; V orthonormality to 10x."""
+    g = PAPER[key]
+    a, sig = synth.paper_test_matrix(g["m"], g["n"])
+    u, s, v = getattr(oracle, alg)(a, *synth.mixing_params(g["n"], 1), 1e-11)
+    err = oracle.spectral_error(a, u, s, v, synth.power_start(g["n"], 7))
+    assert err == pytest.approx(g["spectral_error"], rel=0.1)
+    assert oracle.ortho_error(v) <= 10 * g["max_VtV_minus_I"]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("key,l", [("alg7_l20_i2_m1e4_n2000", 20), ("alg7_l10_i2", 10)])
+def test_paper_alg7(key, l):
+    """PAPER.md:1039 and 1084-1087 (Tables 8 and 10, Algorithm 7): the residual is exactly
+    sigma_{r+1} of Eq. testSl -- 2.64e-12 = sigma_12 (l = 20) and 7.74e-12 = sigma_6 (l = 10) --
+    with the recorded seeds that give the paper's kept ranks (11 and 5)."""
+    g = PAPER[key]
+    a, sig = synth.paper_lowrank_test_matrix(10_000, 2_000, l)
+    seed = g["seed"]
+    u, s, v = oracle.lowrank_svd_tsqr(a, synth.omega(2_000, l, seed), g["i"], l,
+                                      lambda w: synth.mixing_params(w, seed), 1e-11)
+    err = oracle.spectral_error(a, u, s, v, synth.power_start(2_000, 7))
+    assert err == pytest.approx(g["spectral_error"], rel=5e-3)
+    assert abs(err - sig[s.size]) <= 1e-3 * sig[s.size]
+    assert oracle.ortho_error(u) <= 1e-14 and oracle.ortho_error(v) <= 1e-14
