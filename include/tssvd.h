@@ -109,7 +109,9 @@ void tssvd_opts_default(tssvd_opts* opts);
  * Signs: each (u_j, v_j) is flipped so the largest-|.| entry of v_j is positive.
  *
  *   m_local  rows of this rank's shard (>= 0); m = sum over ranks must be >= n
- *   n        columns, 1 <= n <= 256 (odd n allowed)
+ *   n        columns, 1 <= n <= 2048 (odd n allowed; n > 256 runs the wide core: the
+ *            workspace then holds an m_local x n copy of Y~ and the eigen/SVD cores
+ *            are the cooperative multi-CTA solvers)
  *   A        m_local x n, lda >= n, lda EVEN, 16-byte aligned (rows move as
  *            16-byte TMA granules); read-only
  *   U        m_local x n capacity, ldu >= n, ldu even, 16-byte aligned: columns
@@ -153,6 +155,45 @@ int lowrank_svd(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, cons
                 const tssvd_opts* opts, double* U, int64_t ldu, double* sigma, double* V,
                 int64_t ldv, int64_t* rank, void* workspace, size_t workspace_bytes);
 
+/* ---- problem {1} by Algorithms 1 / 2: randomized TSQR-based SVD --
+ * B^* = A Omega^* (every row of A mixed by the random orthogonal Omega = D F S D~ F S~
+ * of Remark 'randomness'), B^* = Q R by TSQR (Householder QR of row blocks,
+ * the stacked R factors QR'd again; multi-rank: the ranks' R all-gathered and factored
+ * identically on every rank), rows of R with |R_jj| < |R_11| wp discarded, SVD of R
+ * (Alg. 2: of T = R R~ after a second TSQR of the kept Q~), U = Q U~, V = Omega^-1 V~.
+ * Same conventions and outputs as tssvd() (signs: largest-|.| entry of v_j positive);
+ * device pointers only (opts->host_io must be 0); opts->orthonormalizations 1 = Alg. 1,
+ * 2 = Alg. 2.
+ *
+ *   n        1 <= n <= 128 (odd n: the last coordinate is left unmixed, R17)
+ *   phases   DEVICE, 2 * (n / 2) doubles: [theta_D (h) ; theta_D~ (h)], h = n / 2,
+ *            D = diag(exp(i theta)); bit-identical on every rank
+ *   perms    DEVICE, 2 * (n / 2) ints: [S (h) ; S~ (h)], permutations of 0..h-1 with
+ *            (S z)_k = z_{S[k]}; bit-identical on every rank
+ *   (F is the unitary DFT of length h acting on the pairs (x_2k, x_2k+1) as complex numbers)
+ */
+int tsqr_svd_workspace_size(const tssvd_comm* comm, int64_t m_local, int64_t n, const tssvd_opts* opts,
+                            size_t* bytes);
+int tsqr_svd(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, const double* A, int64_t lda,
+             const double* phases, const int* perms, const tssvd_opts* opts, double* U, int64_t ldu,
+             double* sigma, double* V, int64_t ldv, int64_t* rank, void* workspace, size_t workspace_bytes);
+
+/* ---- problem {2} by Algorithm 7 ---------------------------------
+ * lowrank_svd() with Algorithm 1 in steps 4 and 6 of Alg. 5 and Algorithm 2 in its
+ * last step and in Alg. 6.  Every factorization gets the random Omega of its width w
+ * (w = l, or the kept rank of the factorization before it): row w - 1 of the tables
+ *   phases   DEVICE, l x l doubles (ld l): row w - 1 = the 2 * (w / 2) phases for width w
+ *   perms    DEVICE, l x l ints (ld l):    row w - 1 = the 2 * (w / 2) permutation entries
+ * (layouts as tsqr_svd's).  Other arguments as lowrank_svd(); device pointers only.
+ */
+int lowrank_tsqr_workspace_size(const tssvd_comm* comm, int64_t m_local, int64_t n, int64_t l,
+                                const tssvd_opts* opts, size_t* bytes);
+int lowrank_svd_tsqr(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, const double* A,
+                     int64_t lda, const double* Omega, int64_t ldo, int64_t l, int iters, int64_t k,
+                     const double* phases, const int* perms, const tssvd_opts* opts, double* U, int64_t ldu,
+                     double* sigma, double* V, int64_t ldv, int64_t* rank, void* workspace,
+                     size_t workspace_bytes);
+
 /* ---- instrumentation ------------------------------------------------------
  * Per-call counters of the last tssvd()/lowrank_svd() on this thread:
  * kernel launches enqueued, Jacobi sweeps of each core, and the kept ranks. */
@@ -165,7 +206,8 @@ typedef enum {
   TSSVD_PASS_UOUT = 5,   /* U = Y~ M (in place)  (Alg. 3 step 6/Alg. 4 st 15) */
   TSSVD_PASS_ALPHA = 6,  /* Y = A Q~             (Alg. 5 steps 3, 8)          */
   TSSVD_PASS_BETA = 7,   /* A^T Q                (Alg. 5 step 5, Alg. 6 st 1) */
-  TSSVD_PASS_JACOBI = 8  /* one-sided Jacobi core (eig / SVD)                 */
+  TSSVD_PASS_JACOBI = 8, /* one-sided Jacobi core (eig / SVD)                 */
+  TSSVD_PASS_TSQR = 9    /* TSQR, Q formed in place (Alg. 1/2 steps 2, 4)     */
 } tssvd_pass_kind;
 typedef struct {
   int64_t kernel_launches;
@@ -203,7 +245,8 @@ int tssvd_matmul_tn(void* stream, int64_t m, int64_t n, int64_t l, const double*
                     size_t workspace_bytes);
 size_t tssvd_matmul_tn_workspace(int64_t m, int64_t n, int64_t l);
 /* Eigendecomposition of a symmetric POSITIVE SEMIDEFINITE B (n x n, ldb; a
- * Gram matrix; 1 <= n <= 256, else TSSVD_EINVAL) by one-sided Jacobi on its
+ * Gram matrix; 1 <= n <= 2048, else TSSVD_EINVAL; n > 256 runs the cooperative
+ * multi-CTA solver) by one-sided Jacobi on its
  * columns: lambda[j] (descending) and the unit eigenvectors as ROWS of Vt
  * (n x n, ldv): Vt[j, :] = v_j.  (For an indefinite B, lambda holds |eigenvalues|.) */
 int tssvd_sym_eig(void* stream, int64_t n, const double* B, int64_t ldb, double* lambda,

@@ -271,6 +271,8 @@ def mix_rows(a: np.ndarray, phases: np.ndarray, perms: np.ndarray, inverse: bool
     n = a.shape[1]
     h = n // 2
     out = a.copy()
+    if h == 0:  # n = 1: the single coordinate is the unmixed last one (reading R17)
+        return out
     z = a[:, 0:2 * h:2] + 1j * a[:, 1:2 * h:2]
     d1, d2 = np.exp(1j * phases[:h]), np.exp(1j * phases[h:2 * h])
     s1, s2 = perms[:h].astype(np.int64), perms[h:2 * h].astype(np.int64)

@@ -32,7 +32,7 @@ class TssvdOpts(ctypes.Structure):
 
 MAX_PASSES = 48
 PASS_KINDS = {1: "gram_x", 2: "xv", 3: "gram_y", 4: "qnorm", 5: "uout", 6: "alpha", 7: "beta",
-              8: "jacobi"}
+              8: "jacobi", 9: "tsqr"}
 
 
 class TssvdStats(ctypes.Structure):
@@ -65,6 +65,16 @@ SIGNATURES = [
     ("lowrank_svd", c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p,
                             c_int64, c_int64, c_int, c_int64, P(TssvdOpts), c_void_p, c_int64,
                             c_void_p, c_void_p, c_int64, P(c_int64), c_void_p, c_size_t]),
+    ("tsqr_svd_workspace_size", c_int, [c_void_p, c_int64, c_int64, P(TssvdOpts), P(c_size_t)]),
+    ("tsqr_svd", c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_void_p,
+                         P(TssvdOpts), c_void_p, c_int64, c_void_p, c_void_p, c_int64, P(c_int64),
+                         c_void_p, c_size_t]),
+    ("lowrank_tsqr_workspace_size", c_int, [c_void_p, c_int64, c_int64, c_int64, P(TssvdOpts),
+                                            P(c_size_t)]),
+    ("lowrank_svd_tsqr", c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p,
+                                 c_int64, c_int64, c_int, c_int64, c_void_p, c_void_p, P(TssvdOpts),
+                                 c_void_p, c_int64, c_void_p, c_void_p, c_int64, P(c_int64), c_void_p,
+                                 c_size_t]),
     ("tssvd_last_stats", c_int, [P(TssvdStats)]),
     ("tssvd_set_pass_timing", c_int, [c_int]),
     ("tssvd_gram", c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_int64,
@@ -148,12 +158,13 @@ def last_stats() -> dict:
 
 def trace(problem: str, nranks: int, m_local: int, n: int, l: int = 0, iters: int = 0, k: int = 0,
           wp: float = 1e-11, passes: int = 2) -> list[str]:
-    """Steps and collectives of one tssvd ('tssvd') / lowrank_svd ('lowrank') call on one of
-    `nranks` ranks, from a plan-only run of the real orchestrator (no GPU needed)."""
+    """Steps and collectives of one tssvd ('tssvd') / lowrank_svd ('lowrank') / tsqr_svd ('tsqr') /
+    lowrank_svd_tsqr ('lowrank_tsqr') call on one of `nranks` ranks, from a plan-only run of the
+    real orchestrator (no GPU needed)."""
     opts = default_opts(wp, passes)
     buf = ctypes.create_string_buffer(1 << 16)
-    check(lib().tssvd_trace(1 if problem == "tssvd" else 2, nranks, m_local, n, l, iters, k,
-                            ctypes.byref(opts), buf, len(buf)))
+    code = {"tssvd": 1, "lowrank": 2, "tsqr": 3, "lowrank_tsqr": 4}[problem]
+    check(lib().tssvd_trace(code, nranks, m_local, n, l, iters, k, ctypes.byref(opts), buf, len(buf)))
     return [t for t in buf.value.decode().split(";") if t]
 
 

@@ -176,6 +176,93 @@ def lowrank_svd(A: torch.Tensor, Omega: torch.Tensor, iters: int, k: int | None 
     return U[:, :q], sigma[:q], V[:, :q]
 
 
+def _mixing(phases: torch.Tensor, perms: torch.Tensor, dev: torch.device):
+    if phases.dtype != torch.float64 or perms.dtype != torch.int32:
+        raise ValueError("phases must be float64 and perms int32")
+    if phases.device != dev or perms.device != dev:
+        raise ValueError("phases / perms must be on A's device")
+    return phases.contiguous(), perms.contiguous()
+
+
+def tsqr_svd(A: torch.Tensor, phases: torch.Tensor, perms: torch.Tensor, wp: float = 1e-11,
+             passes: int = 2, comm: Comm | None = None, max_sweeps: int = 60, inplace: bool = False):
+    """Thin SVD of this rank's shard by Algorithm 2 (passes=2) or 1:
+    the rows mixed by the random Omega = D F S D~ F S~ (Remark 'randomness'; draws
+    `phases` = [theta_D; theta_D~], `perms` = [S; S~], h = n // 2 each, int32), TSQR, SVD of R.
+    Device tensors only; n <= 128.  Returns (U_p, sigma, V) as tssvd()."""
+    _check_tall(A)
+    if A.device.type != "cuda":
+        raise ValueError("tsqr_svd takes device tensors")
+    m, n = A.shape
+    lda = A.stride(0) if m > 0 else n
+    if lda & 1:
+        raise ValueError("A needs an even leading dimension (pad odd widths)")
+    phases, perms = _mixing(phases, perms, A.device)
+    opts = default_opts(wp, passes, max_sweeps)
+    cptr = comm.ptr if comm else None
+    nbytes = ctypes.c_size_t()
+    check(lib().tsqr_svd_workspace_size(cptr, m, n, ctypes.byref(opts), ctypes.byref(nbytes)))
+    ws = _workspace(nbytes.value, A.device)
+    U = A if inplace else torch.empty((m, n + (n & 1)), dtype=torch.float64, device=A.device)
+    sigma = torch.empty(n, dtype=torch.float64, device=A.device)
+    V = torch.empty((n, n), dtype=torch.float64, device=A.device)
+    r = ctypes.c_int64()
+    check(lib().tsqr_svd(cptr, _stream(A.device), m, n, A.data_ptr(), lda, phases.data_ptr(),
+                         perms.data_ptr(), ctypes.byref(opts), U.data_ptr(),
+                         U.stride(0) if m > 0 else n + (n & 1), sigma.data_ptr(), V.data_ptr(), n,
+                         ctypes.byref(r), ws.data_ptr(), ws.numel()))
+    q = r.value
+    return U[:, :q], sigma[:q], V[:, :q]
+
+
+def lowrank_svd_tsqr(A: torch.Tensor, Omega: torch.Tensor, iters: int, phases: torch.Tensor,
+                     perms: torch.Tensor, k: int | None = None, wp: float = 1e-11,
+                     comm: Comm | None = None, max_sweeps: int = 60):
+    """Rank-k approximation by Algorithm 7: Alg. 5 + 6 with the TSQR-based
+    Algorithms 1 / 2.  phases / perms: l x l tables, row w - 1 = the mixing draws for a
+    factorization of width w (float64 / int32, on A's device).  Device tensors only."""
+    _check_tall(A)
+    if A.device.type != "cuda":
+        raise ValueError("lowrank_svd_tsqr takes device tensors")
+    m, n = A.shape
+    l = Omega.shape[1]
+    k = l if k is None else k
+    if Omega.device != A.device or Omega.dtype != torch.float64 or Omega.stride(1) != 1:
+        raise ValueError("Omega must be float64 on A's device with unit column stride")
+    phases, perms = _mixing(phases, perms, A.device)
+    if tuple(phases.shape) != (l, l) or tuple(perms.shape) != (l, l):
+        raise ValueError("phases / perms must be l x l tables")
+    opts = default_opts(wp, 2, max_sweeps)
+    cptr = comm.ptr if comm else None
+    nbytes = ctypes.c_size_t()
+    check(lib().lowrank_tsqr_workspace_size(cptr, m, n, l, ctypes.byref(opts), ctypes.byref(nbytes)))
+    ws = _workspace(nbytes.value, A.device)
+    kk = max(k, 1)
+    ldu = kk + (kk & 1)
+    U = torch.empty((m, ldu), dtype=torch.float64, device=A.device)
+    sigma = torch.empty(kk, dtype=torch.float64, device=A.device)
+    V = torch.empty((n, kk), dtype=torch.float64, device=A.device)
+    r = ctypes.c_int64()
+    check(lib().lowrank_svd_tsqr(cptr, _stream(A.device), m, n, A.data_ptr(),
+                                 A.stride(0) if m > 0 else n, Omega.data_ptr(), Omega.stride(0), l,
+                                 iters, k, phases.data_ptr(), perms.data_ptr(), ctypes.byref(opts),
+                                 U.data_ptr(), ldu, sigma.data_ptr(), V.data_ptr(), kk,
+                                 ctypes.byref(r), ws.data_ptr(), ws.numel()))
+    q = r.value
+    return U[:, :q], sigma[:q], V[:, :q]
+
+
+def mixing_tables(mixes, l: int, device) -> tuple[torch.Tensor, torch.Tensor]:
+    """l x l tables for lowrank_svd_tsqr from mixes(w) -> (phases, perms) (row w - 1: width w)."""
+    ph = torch.zeros((l, l), dtype=torch.float64)
+    pm = torch.zeros((l, l), dtype=torch.int32)
+    for w in range(1, l + 1):
+        a, b = mixes(w)
+        ph[w - 1, : len(a)] = torch.as_tensor(a, dtype=torch.float64)
+        pm[w - 1, : len(b)] = torch.as_tensor(b, dtype=torch.int32)
+    return ph.to(device), pm.to(device)
+
+
 # ---- kernel-level building blocks (parity tests / microbenchmarks) --------
 def gram(X: torch.Tensor) -> torch.Tensor:
     """X^T X over the local rows (Alg. 3 step 1 before aggregation)."""

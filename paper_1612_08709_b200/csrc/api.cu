@@ -816,6 +816,120 @@ int64_t core_rank(const CoreOut& o, const Finish& f) {
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+// ---------------------------------------------------------- TSQR cores ----
+// Algorithms 1 / 2: the randomized TSQR-based SVD of a tall-skinny X (w <= 128).
+struct TsqrCore {
+  int w = 0, P = 1;
+  double *M0, *Mg, *R1, *R2, *T, *svo, *sv, *work, *Rloc, *Rall, *work2;
+  int *mask1, *mask2;
+  void alloc(Arena& a, int64_t m, int ww, int nranks) {
+    w = ww;
+    P = std::max(nranks, 1);
+    M0 = a.get<double>((size_t)w * w);
+    Mg = a.get<double>(gemm_nn_m_doubles(w, w));
+    R1 = a.get<double>((size_t)w * w);
+    R2 = a.get<double>((size_t)w * w);
+    T = a.get<double>((size_t)w * w);
+    svo = a.get<double>((size_t)2 * w * w);
+    sv = a.get<double>(w);
+    work = a.get<double>(tsqr_workspace_doubles(std::max<int64_t>(m, 1), w));
+    Rloc = a.get<double>((size_t)w * w);
+    Rall = a.get<double>((size_t)P * w * w);
+    work2 = a.get<double>(tsqr_workspace_doubles((int64_t)P * w, w));
+    mask1 = a.get<int>(w + 1);
+    mask2 = a.get<int>(w + 1);
+  }
+};
+
+// TSQR of X (m_local x w, in place -> Q) with R (w x w, replicated) to R_out.  Row-sharded
+// (dist): each rank's TSQR gives Q_p R_p; the R_p are all-gathered (P w x w, rank order) and
+// factored again, identically on every rank: [R_0; ...; R_P-1] = Q' R; Q_p <- Q_p Q'_p (the
+// rank's w rows of Q') -- the top of the TSQR tree.
+void tsqr_run(Ctx& c, TsqrCore& b, double* X, int64_t ldx, int64_t m_local, int w, bool dd, double* R_out) {
+  cudaStream_t s = c.s;
+  step("tsqr:%d", w);
+  {
+    Pass t(s, TSSVD_PASS_TSQR, 4.0 * m_local * w * w, 16.0 * m_local * w);
+    KL(launch_tsqr(X, ldx, m_local, w, dd ? b.Rloc : R_out, b.work, s));
+  }
+  ++g_stats.a_passes;
+  if (!dd) return;
+  step("allgather:R:%d", w * w);
+  if (!g_dry)
+    NC(ncclAllGather(b.Rloc, b.Rall, (size_t)w * w, ncclDouble, c.comm->nccl, s));
+  KL(launch_tsqr(b.Rall, w, (int64_t)c.comm->nranks * w, w, R_out, b.work2, s));
+  step("tsqr_top");
+  KS(rows_to_m(b.Rall + (size_t)c.comm->rank * w * w, w, w, w, b.Mg, smem_ld(w), mrows_for(w), s));
+  KL(launch_gemm_nn(X, ldx, m_local, w, b.Mg, w, X, ldx, nullptr, nullptr, s));
+}
+
+// Alg. 1 (passes = 1) or Alg. 2 (passes = 2) on X (m_local x w, ldx),
+// U (may alias X) receives U[:, :r]; sigma[:r], V (w x r, ldv) replicated.  The width of the
+// factorization is w, or the device count *wdev <= w (columns past it are zero: the draws of
+// the random Omega are then row *wdev - 1 of the tables, ld ldp).  Every decision stays on the
+// device (launches sized by w, zero columns past the kept rank).
+CoreOut tsqr_core(Ctx& c, TsqrCore& b, const double* X, int64_t ldx, int64_t m_local, int w, const int* wdev,
+                  const double* ph, const int* pm, int ldp, int passes, bool dist, double* U, int64_t ldu,
+                  double* sigma, double* V, int64_t ldv) {
+  cudaStream_t s = c.s;
+  Ctx cd = c;
+  if (!dist) cd.comm = nullptr;
+  const bool dd = cd.dist();
+  step("tsqr_core:%s:%d:%d", dist ? "sharded" : "local", passes, w);
+  // Step 1 (P:527-529 / P:567-569): B^* = A Omega^* -- every row of A mixed by Omega.
+  step("mix");
+  const double* ph0 = (!wdev && ldp > 0) ? ph + (size_t)(w - 1) * ldp : ph;
+  const int* pm0 = (!wdev && ldp > 0) ? pm + (size_t)(w - 1) * ldp : pm;
+  KL(launch_mix_matrix(ph0, pm0, ldp, wdev, w, w, b.M0, w, s));
+  KS(rows_to_m(b.M0, w, w, w, b.Mg, smem_ld(w), mrows_for(w), s));
+  {
+    Pass t(s, TSSVD_PASS_XV, 2.0 * m_local * w * w, 16.0 * m_local * w);
+    KL(launch_gemm_nn(X, ldx, m_local, w, b.Mg, w, U, ldu, nullptr, nullptr, s));
+  }
+  ++g_stats.a_passes;
+  // Step 2 (P:531-532 / P:571-573): B^* = Q R (Q~ R~) by TSQR, Q in place in U.
+  tsqr_run(cd, b, U, ldu, m_local, w, dd, b.R1);
+  // Step 3 (P:534-538 / P:575-579): discard rows of R with |R_jj| < |R_11| wp.
+  step("discard:1");
+  const int s1 = c.next_slot();
+  KL(launch_r_discard(b.R1, w, c.wp, c.slot(s1), b.mask1, s));
+  int slot = s1;
+  const double* K = b.R1;
+  if (passes == 2) {
+    // Step 4: Q~ (kept columns) = Q R.
+    step("zero_cols");
+    KL(launch_zero_cols(U, ldu, m_local, w, b.mask1, s));
+    tsqr_run(cd, b, U, ldu, m_local, w, dd, b.R2);
+    // Step 5: discard.  Step 6: T = R R~.
+    step("discard:2");
+    const int s2 = c.next_slot();
+    KL(launch_r_discard(b.R2, w, c.wp, c.slot(s2), b.mask2, s));
+    KL(launch_tri_mul(b.R2, b.R1, w, b.T, s));
+    K = b.T;
+    slot = s2;
+  }
+  // Step 4 / 7 (P:540-543 / P:593-596): R (T) = U~ Sigma V~^* by one-sided Jacobi on the columns
+  // of K = R^T (rows of R): K J = P Sigma  =>  U~ = J, V~ = P.
+  step("svd:R");
+  {
+    Pass t(s, TSSVD_PASS_JACOBI, 0, 0);
+    KL(launch_jacobi_svd(K, w, w, w, jacobi_tol(w), c.max_sweeps, b.svo, 2 * w, b.sv, c.next_info(), s));
+  }
+  // Step 5-6 / 8-9 (P:545-549 / P:598-602): V = Omega^-1 V~, U = Q U~ (in place), signs (R5).
+  step("tsqr_out");
+  KS(fill(b.Mg, (int64_t)mrows_for(w) * smem_ld(w), 0.0, s));
+  KL(launch_tsqr_out(b.svo, w, b.sv, b.M0, c.slot(slot) + kSlotR, sigma, V, ldv, b.Mg, smem_ld(w), s));
+  step("uout:%d", w);
+  {
+    Pass t(s, TSSVD_PASS_UOUT, 2.0 * m_local * w * w, 16.0 * m_local * w);
+    KL(launch_gemm_nn(U, ldu, m_local, w, b.Mg, w, U, ldu, nullptr, nullptr, s));
+  }
+  CoreOut out;
+  out.bound = w;
+  out.slot = slot;
+  return out;
+}
+
 
 void check_opts(const tssvd_opts* o) {
   if (!o) fail(TSSVD_EINVAL, "opts is NULL");
@@ -973,18 +1087,25 @@ void tssvd_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, cons
 // ------------------------------------------------------------- low rank --
 struct LrPlan {
   Core tall, small;
+  TsqrCore tq_tall, tq_small;  // Alg. 7 (method 1)
   int* ctl;
   double *Qt, *Y, *Z, *tn, *Ut, *sig_tmp, *v_scr, *sig_scr, *Mfin, *sk;
   double *a_stage, *a_stage2, *o_stage, *u_stage, *s_stage, *vo_stage;
   int lp, ldzmax;
 };
 
-size_t plan_lowrank(Arena& a, LrPlan& p, int64_t m_local, int n, int l, const tssvd_opts* o) {
+size_t plan_lowrank(Arena& a, LrPlan& p, int64_t m_local, int n, int l, const tssvd_opts* o, int method = 0,
+                    int nranks = 1) {
   p.lp = (l + 1) & ~1;
   p.ldzmax = pad8(l);
   p.ctl = a.get<int>(kCtlInts);
-  p.tall.alloc(a, m_local, l);
-  p.small.alloc(a, n, l);
+  if (method == 0) {
+    p.tall.alloc(a, m_local, l);
+    p.small.alloc(a, n, l);
+  } else {
+    p.tq_tall.alloc(a, m_local, l, nranks);
+    p.tq_small.alloc(a, n, l, 1);
+  }
   p.Qt = a.get<double>(gemm_nn_m_doubles(n, l));
   p.Y = a.get<double>((size_t)std::max<int64_t>(m_local, 1) * p.lp);
   p.Z = a.get<double>((size_t)n * p.ldzmax);
@@ -1091,11 +1212,16 @@ int tn_pass(Ctx& c, LrPlan& p, ASource& src, int64_t m_local, int n, int r) {
 void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, const double* A,
                   int64_t lda, const double* Omega, int64_t ldo, int64_t l, int iters, int64_t k,
                   const tssvd_opts* opts, double* U, int64_t ldu, double* sigma, double* V,
-                  int64_t ldv, int64_t* rank, void* ws, size_t ws_bytes) {
+                  int64_t ldv, int64_t* rank, void* ws, size_t ws_bytes, int method = 0,
+                  const double* mph = nullptr, const int* mpm = nullptr) {
+  // method 0: Algorithm 8 (Gram-based cores); 1: Algorithm 7 (TSQR-based cores, the random
+  // mixing draws per width in the tables mph / mpm, ld l)
   g_stats = tssvd_stats{};
   check_opts(opts);
   if (m_local < 0) fail(TSSVD_EINVAL, "m_local < 0");
   if (n < 2) fail(TSSVD_EINVAL, "n = %lld must be >= 2", (long long)n);
+  if (method == 1 && opts->host_io != 0) fail(TSSVD_EINVAL, "lowrank_svd_tsqr takes device pointers (host_io 0)");
+  if (method == 1 && (!mph || !mpm)) fail(TSSVD_EINVAL, "phases / perms tables are NULL");
   if (lda < n || (opts->host_io != 1 && (lda & 1)))
     fail(TSSVD_EINVAL, "lda must be even and >= n (16-byte TMA row strides)");
   if (l < 1 || l > 128 || l >= n) fail(TSSVD_EINVAL, "need 0 < l < min(m, n) and l <= 128 (l = %lld)", (long long)l);
@@ -1120,13 +1246,15 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
   a.cap = ws_bytes;
   a.dry = false;
   LrPlan p;
-  plan_lowrank(a, p, m_local, (int)n, (int)l, opts);
+  plan_lowrank(a, p, m_local, (int)n, (int)l, opts, method, comm ? comm->nranks : 1);
   c.ctl = p.ctl;
   const bool use_graph = !hio && !g_dry && graphs_on();
   GraphKey key{};
   if (use_graph) {
-    const void* ps[10] = {comm, A, Omega, U, sigma, V, ws, stream, nullptr, nullptr};
-    const int64_t vs[10] = {m_local, n, lda, ldo, l, iters, k, ldu, ldv, (int64_t)ws_bytes ^ ((int64_t)opts->max_jacobi_sweeps << 48) ^ ((int64_t)g_timing << 60)};
+    const void* ps[10] = {comm, A, Omega, U, sigma, V, ws, stream, mph, mpm};
+    const int64_t vs[10] = {m_local, n, lda, ldo, l, iters, k, ldu, ldv,
+                            (int64_t)ws_bytes ^ ((int64_t)opts->max_jacobi_sweeps << 48) ^
+                                ((int64_t)method << 56) ^ ((int64_t)g_timing << 60)};
     std::memcpy(key.p, ps, sizeof ps);
     std::memcpy(key.v, vs, sizeof vs);
     key.wp = opts->working_precision;
@@ -1207,6 +1335,17 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
     });
     ++g_stats.a_passes;
   };
+  // The factorizations: Alg. 3 / 4 (method 0) or Alg. 1 / 2 (method 1).  wprev: the device
+  // count of the previous factorization's kept rank = the width of the next one's input (its
+  // columns past it are zero; Alg. 1/2 draw their Omega for that width).
+  const int* wprev = nullptr;
+  auto fact = [&](Core& cb, TsqrCore& tb, double* X, int64_t ldx, int64_t rows, int w, int passes, bool dist,
+                  double* sg, double* Vv) -> CoreOut {
+    CoreOut o = method == 0 ? core(c, cb, X, ldx, rows, w, passes, dist, X, ldx, sg, Vv, Lc, true)
+                            : tsqr_core(c, tb, X, ldx, rows, w, wprev, mph, mpm, Lc, passes, dist, X, ldx, sg, Vv, Lc);
+    wprev = c.slot(o.slot) + kSlotR;
+    return o;
+  };
   // Every decision stays on the device (no host round trip until the end): the
   // launches are sized by the block width l, and columns past a kept rank are zeros.
   // Alg. 5 step 1: Q~_0 = Omega.
@@ -1214,22 +1353,22 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
   for (int it = 0; it < iters; ++it) {
     // step 3: Y_j = A Q~_{j-1}
     alpha();
-    // step 4: Y_j = Q_j R_j by Alg. 3 (Q_j = U, in place in Y)
-    core(c, p.tall, p.Y, p.lp, m_local, Lc, 1, true, p.Y, p.lp, p.sig_scr, p.v_scr, Lc, true);
+    // step 4: Y_j = Q_j R_j by Alg. 3 / Alg. 1 (Q_j = U, in place in Y)
+    fact(p.tall, p.tq_tall, p.Y, p.lp, m_local, Lc, 1, true, p.sig_scr, p.v_scr);
     // step 5: Y~_j = A^* Q_j
     const int ldz = tn_pass(c, p, src, m_local, N, Lc);
-    // step 6: Y~_j = Q~_j R~_j by Alg. 3 on the replicated n x l matrix
-    core(c, p.small, p.Z, ldz, N, Lc, 1, false, p.Z, ldz, p.sig_scr, p.v_scr, Lc, true);
+    // step 6: Y~_j = Q~_j R~_j by Alg. 3 / Alg. 1 on the replicated n x l matrix
+    fact(p.small, p.tq_small, p.Z, ldz, N, Lc, 1, false, p.sig_scr, p.v_scr);
     step("qt");
     KS(rows_to_m(p.Z, ldz, N, Lc, p.Qt, smem_ld(Lc), mrows_for(N), c.s));
   }
-  // step 8: Y = A Q~_i; step 9: Y = Q R by Alg. 4
+  // step 8: Y = A Q~_i; step 9: Y = Q R by Alg. 4 / Alg. 2
   alpha();
-  const CoreOut o3 = core(c, p.tall, p.Y, p.lp, m_local, Lc, 2, true, p.Y, p.lp, p.sig_scr, p.v_scr, Lc, true);
+  const CoreOut o3 = fact(p.tall, p.tq_tall, p.Y, p.lp, m_local, Lc, 2, true, p.sig_scr, p.v_scr);
   // Alg. 6 step 1: B^T = A^* Q
   const int ldz = tn_pass(c, p, src, m_local, N, o3.bound);
-  // Alg. 6 step 2: B^T = V Sigma U~^* by Alg. 4 (reading R6); V in place in Z
-  const CoreOut o4 = core(c, p.small, p.Z, ldz, N, o3.bound, 2, false, p.Z, ldz, p.sig_tmp, p.Ut, Lc, true);
+  // Alg. 6 step 2: B^T = V Sigma U~^* by Alg. 4 / Alg. 2 (reading R6); V in place in Z
+  const CoreOut o4 = fact(p.small, p.tq_small, p.Z, ldz, N, o3.bound, 2, false, p.sig_tmp, p.Ut);
   step("canon");
   KS(canon_lowrank(p.Z, ldz, N, p.Ut, Lc, o3.bound, c.slot(o4.slot) + kSlotR, o4.bound, c.s));
   const int kk = (int)std::min<int64_t>(k, o4.bound);
@@ -1288,6 +1427,64 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
     }
     throw;
   }
+}
+
+// ------------------------------------------------ Alg. 1 / 2 (tsqr_svd) --
+struct TqPlan {
+  TsqrCore core;
+  int* ctl;
+};
+
+size_t plan_tsqr(Arena& a, TqPlan& p, int64_t m_local, int n, int nranks) {
+  p.ctl = a.get<int>(kCtlInts);
+  p.core.alloc(a, m_local, n, nranks);
+  return a.off;
+}
+
+constexpr int kTsqrMax = 128;
+
+void tsqr_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, const double* A, int64_t lda,
+               const double* phases, const int* perms, const tssvd_opts* opts, double* U, int64_t ldu,
+               double* sigma, double* V, int64_t ldv, int64_t* rank, void* ws, size_t ws_bytes) {
+  g_stats = tssvd_stats{};
+  check_opts(opts);
+  if (opts->host_io != 0) fail(TSSVD_EINVAL, "tsqr_svd takes device pointers (host_io 0)");
+  if (m_local < 0) fail(TSSVD_EINVAL, "m_local < 0");
+  if (n < 1 || n > kTsqrMax) fail(TSSVD_EINVAL, "n = %lld must be in [1, %d]", (long long)n, kTsqrMax);
+  if (opts->orthonormalizations != 1 && opts->orthonormalizations != 2)
+    fail(TSSVD_EINVAL, "orthonormalizations must be 1 or 2");
+  if (lda < n || (lda & 1) || ldu < n || (ldu & 1)) fail(TSSVD_EINVAL, "lda and ldu must be even and >= n");
+  if (ldv < n) fail(TSSVD_EINVAL, "ldv < n");
+  if (!rank) fail(TSSVD_EINVAL, "rank is NULL");
+  if (n >= 2 && (!phases || !perms)) fail(TSSVD_EINVAL, "phases / perms are NULL");
+  if (m_local > 0 && (!aligned16(A) || !aligned16(U))) fail(TSSVD_EINVAL, "A and U must be 16-byte aligned");
+  if (!ws || !aligned16(ws)) fail(TSSVD_EINVAL, "workspace NULL or misaligned");
+  set_device(comm);
+  Ctx c;
+  c.comm = comm;
+  c.s = static_cast<cudaStream_t>(stream);
+  c.wp = opts->working_precision;
+  c.max_sweeps = opts->max_jacobi_sweeps;
+  Arena a;
+  a.base = static_cast<char*>(ws);
+  a.cap = ws_bytes;
+  a.dry = false;
+  TqPlan p;
+  plan_tsqr(a, p, m_local, (int)n, comm ? comm->nranks : 1);
+  c.ctl = p.ctl;
+  step("tsqr_svd:%d", opts->orthonormalizations);
+  CUR(cudaMemsetAsync(c.ctl, 0, kCtlInts * sizeof(int), c.s));
+  const int64_t m_now = global_rows(c, m_local);
+  if (m_now >= 0 && m_now < n)
+    fail(TSSVD_EINVAL, "m = %lld < n = %lld (the matrix must be tall, P:98-104)", (long long)m_now, (long long)n);
+  const CoreOut o = tsqr_core(c, p.core, A, lda, m_local, (int)n, nullptr, phases, perms, 0,
+                              opts->orthonormalizations, true, U, ldu, sigma, V, ldv);
+  Finish f;
+  finish(c, f);
+  if (c.dist() && !g_dry && f.m < n)
+    fail(TSSVD_EINVAL, "m = %lld < n = %lld (the matrix must be tall, P:98-104)", (long long)f.m, (long long)n);
+  g_timer.resolve();
+  *rank = core_rank(o, f);
 }
 
 }  // namespace
@@ -1434,6 +1631,50 @@ int lowrank_svd(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, cons
   });
 }
 
+int tsqr_svd_workspace_size(const tssvd_comm* comm, int64_t m_local, int64_t n, const tssvd_opts* opts,
+                            size_t* bytes) {
+  return guarded([&] {
+    check_opts(opts);
+    if (m_local < 0 || n < 1 || n > kTsqrMax) fail(TSSVD_EINVAL, "bad sizes (1 <= n <= %d)", kTsqrMax);
+    if (!bytes) fail(TSSVD_EINVAL, "bytes is NULL");
+    Arena a;
+    TqPlan p;
+    *bytes = plan_tsqr(a, p, m_local, (int)n, comm ? comm->nranks : 1) + 256;
+  });
+}
+
+int tsqr_svd(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, const double* A, int64_t lda,
+             const double* phases, const int* perms, const tssvd_opts* opts, double* U, int64_t ldu,
+             double* sigma, double* V, int64_t ldv, int64_t* rank, void* workspace, size_t workspace_bytes) {
+  return guarded([&] {
+    tsqr_impl(comm, stream, m_local, n, A, lda, phases, perms, opts, U, ldu, sigma, V, ldv, rank, workspace,
+              workspace_bytes);
+  });
+}
+
+int lowrank_tsqr_workspace_size(const tssvd_comm* comm, int64_t m_local, int64_t n, int64_t l,
+                                const tssvd_opts* opts, size_t* bytes) {
+  return guarded([&] {
+    check_opts(opts);
+    if (m_local < 0 || n < 2 || l < 1 || l > 128 || l >= n) fail(TSSVD_EINVAL, "bad sizes");
+    if (!bytes) fail(TSSVD_EINVAL, "bytes is NULL");
+    Arena a;
+    LrPlan p;
+    *bytes = plan_lowrank(a, p, m_local, (int)n, (int)l, opts, 1, comm ? comm->nranks : 1) + 256;
+  });
+}
+
+int lowrank_svd_tsqr(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, const double* A,
+                     int64_t lda, const double* Omega, int64_t ldo, int64_t l, int iters, int64_t k,
+                     const double* phases, const int* perms, const tssvd_opts* opts, double* U, int64_t ldu,
+                     double* sigma, double* V, int64_t ldv, int64_t* rank, void* workspace,
+                     size_t workspace_bytes) {
+  return guarded([&] {
+    lowrank_impl(comm, stream, m_local, n, A, lda, Omega, ldo, l, iters, k, opts, U, ldu, sigma, V, ldv, rank,
+                 workspace, workspace_bytes, 1, phases, perms);
+  });
+}
+
 int tssvd_trace(int problem, int nranks, int64_t m_local, int64_t n, int64_t l, int iters, int64_t k,
                 const tssvd_opts* opts, char* buf, size_t buf_len) {
   struct DryScope {  // restores normal operation however the run ends
@@ -1444,7 +1685,8 @@ int tssvd_trace(int problem, int nranks, int64_t m_local, int64_t n, int64_t l, 
     ~DryScope() { g_dry = false; }
   };
   return guarded([&] {
-    if (problem != 1 && problem != 2) fail(TSSVD_EINVAL, "problem must be 1 (tssvd) or 2 (lowrank_svd)");
+    if (problem < 1 || problem > 4)
+      fail(TSSVD_EINVAL, "problem must be 1 (tssvd), 2 (lowrank_svd), 3 (tsqr_svd) or 4 (lowrank_svd_tsqr)");
     if (nranks < 1 || !buf || buf_len == 0) fail(TSSVD_EINVAL, "bad trace arguments");
     check_opts(opts);
     tssvd_opts o = *opts;
@@ -1460,12 +1702,16 @@ int tssvd_trace(int problem, int nranks, int64_t m_local, int64_t n, int64_t l, 
     {
       DryScope dry;
       const int64_t ld = even(n), lk = even(std::max<int64_t>(k, 1));
+      tssvd_comm* fcp = nranks > 1 ? &fc : nullptr;
+      const int* ifake = reinterpret_cast<const int*>(fake);
       if (problem == 1)
-        tssvd_impl(nranks > 1 ? &fc : nullptr, nullptr, m_local, n, fake, ld, &o, fake, ld, fake, fake, n, &rank,
-                   fws, fws_bytes);
+        tssvd_impl(fcp, nullptr, m_local, n, fake, ld, &o, fake, ld, fake, fake, n, &rank, fws, fws_bytes);
+      else if (problem == 3)
+        tsqr_impl(fcp, nullptr, m_local, n, fake, ld, fake, ifake, &o, fake, ld, fake, fake, n, &rank, fws,
+                  fws_bytes);
       else
-        lowrank_impl(nranks > 1 ? &fc : nullptr, nullptr, m_local, n, fake, ld, fake, l, l, iters, k, &o, fake,
-                     lk, fake, fake, k, &rank, fws, fws_bytes);
+        lowrank_impl(fcp, nullptr, m_local, n, fake, ld, fake, l, l, iters, k, &o, fake, lk, fake, fake, k, &rank,
+                     fws, fws_bytes, problem == 4 ? 1 : 0, fake, ifake);
     }
     if (g_trace.size() + 1 > buf_len) fail(TSSVD_ENOMEM, "trace needs %zu bytes", g_trace.size() + 1);
     std::memcpy(buf, g_trace.c_str(), g_trace.size() + 1);

@@ -85,4 +85,19 @@ cudaError_t launch_jacobi_svd_wide(const double* cols, int ldc, int N, int dot, 
                                    double* out, int ldout, double* vals, int* info, double* work,
                                    cudaStream_t s);
 
+// ---- Algorithms 1 / 2 (tsqr.cu), n <= 128 ----
+// Omega^T (wb x wb, ld ldm; row i = Omega e_i) for width *wdev (device, draws at row w-1 of the
+// tables, ld ldp) or wconst (wdev null: the draws at phases / perms); zero past the width.
+cudaError_t launch_mix_matrix(const double* phases, const int* perms, int ldp, const int* wdev, int wconst, int wb,
+                              double* M, int ldm, cudaStream_t s);
+// TSQR in place: X (rows x n, ldx) <- Q, R (n x n, row-major) to R_out; work: tsqr_workspace_doubles.
+int tsqr_block_rows(int n);
+size_t tsqr_workspace_doubles(int64_t rows, int n);
+cudaError_t launch_tsqr(double* X, int64_t ldx, int64_t rows, int n, double* R_out, double* work, cudaStream_t s);
+cudaError_t launch_r_discard(double* R, int w, double wp, int* slot, int* mask, cudaStream_t s);
+cudaError_t launch_zero_cols(double* X, int64_t ldx, int64_t m, int w, const int* mask, cudaStream_t s);
+cudaError_t launch_tri_mul(const double* R2, const double* R1, int w, double* T, cudaStream_t s);
+cudaError_t launch_tsqr_out(const double* svo, int w, const double* vals, const double* M0, const int* rr,
+                            double* sigma, double* V, int64_t ldv, double* Mg, int ldm, cudaStream_t s);
+
 }  // namespace tsk
