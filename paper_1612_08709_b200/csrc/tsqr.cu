@@ -7,7 +7,7 @@
 //     as complex numbers; for odd n the last coordinate is left unmixed, reading R17).  Row i of
 //     the output is Omega e_i, i.e. the output is Omega^T, so B^* = A Omega^T is a GEMM.
 //   * TSQR: leaf Householder QR of row blocks of b >= n rows, one CTA per block with the block
-//     in shared memory (LAPACK dgeqr2 order: column by column, reflector H = I - tau v v^T with
+//     in registers (LAPACK dgeqr2 order: column by column, reflector H = I - tau v v^T with
 //     v_j = 1), the explicit Q of the block formed in place (dorg2r order); the blocks' R
 //     factors are stacked and factored the same way, recursively, and the final Q of a level
 //     is its blocks' Q times the matching rows of the level above (k_block_mul).
@@ -20,8 +20,6 @@
 #include "kernels.h"
 
 namespace tsk {
-
-static constexpr int QT = 512;  // threads per CTA
 
 // ------------------------------------------------------------------ Omega --
 // Output row i = Omega e_i (M[i][j], ld ldm): z = complex pairs of e_i; z <- S~ z; z <- F z;
@@ -81,128 +79,334 @@ __global__ void __launch_bounds__(256) k_mix_matrix(const double* phases, const 
 }
 
 // ------------------------------------------------------ leaf Householder QR --
-// Block `blk` of X (rows [blk*b, min(rows, (blk+1)*b)) x n, ld ldx): R (kmax x n, upper, row-major,
-// ld n) to R + roff(blk) * n, the explicit Q (k x kmax) back into the block, columns past kmax zero.
-// roff(blk) = sum of kmax over the earlier blocks = blk * n (every block but the last has >= n rows).
-__global__ void __launch_bounds__(QT, 1) k_leaf_qr(double* X, int64_t ldx, int64_t rows, int n, int b,
-                                                  double* R) {
-  extern __shared__ double xs[];  // [b][n + 1]
-  __shared__ double s_red[QT / 32];
-  __shared__ double s_tau[128];
-  __shared__ double s_par[2];
-  const int ldsm = n + 1;
-  const int64_t r0 = (int64_t)blockIdx.x * b;
-  const int k = (int)min((int64_t)b, rows - r0);
-  const int kmax = min(k, n);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int e = tid; e < k * n; e += QT) {
-    const int i = e / n, c = e % n;
-    xs[i * ldsm + c] = X[(r0 + i) * ldx + c];
-  }
-  __syncthreads();
-  // ---- Householder QR (dgeqr2 order)
-  for (int j = 0; j < kmax; ++j) {
-    double s = 0.0;
-    for (int i = j + 1 + tid; i < k; i += QT) s = fma(xs[i * ldsm + j], xs[i * ldsm + j], s);
+// One CTA per block of B = 4 RPT rows, the block REGISTER-resident: thread (c, g) (t = 4 c + g)
+// holds column c at the rows i = 4 q + g (q < RPT; interleaved, so every thread keeps the same
+// share of active rows as the factorization advances).  The four threads of a column are
+// adjacent lanes (column norms and dot products reduce with two shuffles); the four columns of a
+// panel [4P, 4P + 4) are one half-warp.
+// Blocked Householder (LAPACK dgeqrf / dorgqr with panels of 4, compact WY H_p..H_p+3 =
+// I - V T V^T, T upper triangular as dlarft):
+//   QR, per panel: its half-warp factors the 4 columns (dgeqr2 order: dlarfg beta =
+//   -sign(alpha) ||x||, tau = (beta - alpha) / beta, v = x / (alpha - beta), v_j = 1; each
+//   reflector applied to the panel's later columns), builds T and publishes V; one CTA barrier;
+//   every later column c: C <- (I - V T^T V^T) C.
+//   Q, panels last to first: the panel's columns reset to e_c, then every column c >= 4P:
+//   C <- (I - V T V^T) C  (Q = H_0 .. H_kmax-1 [I; 0]; one barrier per panel).
+// V in shared memory: vp[g (4 RPT + 4) + 4 q + k] = v_k at row 4q + g (a thread's row: 32 bytes;
+// the pad puts the four groups of a warp on different banks).
+// Block `blk`: rows [blk B, min(rows, (blk + 1) B)); R (kmax x n, upper, row-major ld n) to
+// R + blk n n, the explicit Q (k x kmax) back in place, columns past kmax zero.
+
+// publish slot k of panel V from my column (col): v_i = x (i > col), 1 (i == col), 0 (i < col);
+// an absent reflector (col >= kmax) publishes zeros
+template <int RPT>
+__device__ __forceinline__ void pan_publish(const double (&x)[RPT], int col, bool present, int g, int k,
+                                            double* vp) {
+  double* row = vp + (size_t)g * (RPT * 4 + 4) + k;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) s_red[warp] = s;
-    __syncthreads();
-    if (tid == 0) {
-      double sig2 = 0.0;
-      for (int w = 0; w < QT / 32; ++w) sig2 += s_red[w];
-      const double alpha = xs[j * ldsm + j];
-      double tau = 0.0, scale = 0.0, beta = alpha;
-      if (sig2 > 0.0) {  // (dlarfg; sig2 == 0: H = I)
-        const double nrm = sqrt(fma(alpha, alpha, sig2));
-        beta = alpha >= 0.0 ? -nrm : nrm;
-        tau = (beta - alpha) / beta;
-        scale = 1.0 / (alpha - beta);
-      }
-      s_tau[j] = tau;
-      s_par[0] = scale;
-      s_par[1] = beta;
-    }
-    __syncthreads();
-    const double tau = s_tau[j], scale = s_par[0];
-    if (tau != 0.0)
-      for (int i = j + 1 + tid; i < k; i += QT) xs[i * ldsm + j] *= scale;  // v (v_j = 1 implicit)
-    __syncthreads();
-    if (tid == 0) xs[j * ldsm + j] = s_par[1];  // R_jj
-    // H_j to the trailing columns: one warp per column (lanes over rows, fixed-order sums)
-    if (tau != 0.0)
-      for (int c = j + 1 + warp; c < n; c += QT / 32) {
-        double w = 0.0;
-        for (int i = j + 1 + lane; i < k; i += 32) w = fma(xs[i * ldsm + j], xs[i * ldsm + c], w);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-        w += xs[j * ldsm + c];  // v_j = 1
-        const double tw = tau * w;
-        if (lane == 0) xs[j * ldsm + c] -= tw;
-        for (int i = j + 1 + lane; i < k; i += 32) xs[i * ldsm + c] = fma(-tw, xs[i * ldsm + j], xs[i * ldsm + c]);
-      }
-    __syncthreads();
-  }
-  // ---- R out (rows 0..kmax-1, upper triangle; below-diagonal zero)
-  double* Rb = R + (size_t)blockIdx.x * n * n;
-  for (int e = tid; e < kmax * n; e += QT) {
-    const int i = e / n, c = e % n;
-    Rb[(size_t)i * n + c] = c >= i ? xs[i * ldsm + c] : 0.0;
-  }
-  __syncthreads();
-  // ---- explicit Q in place (dorg2r order): columns kmax-1 .. 0
-  for (int j = kmax - 1; j >= 0; --j) {
-    const double tau = s_tau[j];
-    if (j < kmax - 1) {  // H_j to Q's columns j+1.., rows j..
-      for (int c = j + 1 + warp; c < kmax; c += QT / 32) {
-        double w = 0.0;
-        for (int i = j + 1 + lane; i < k; i += 32) w = fma(xs[i * ldsm + j], xs[i * ldsm + c], w);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-        w += xs[j * ldsm + c];  // row j of column c is 0 here (set when c was formed), v_j = 1
-        const double tw = tau * w;
-        if (lane == 0) xs[j * ldsm + c] -= tw;
-        for (int i = j + 1 + lane; i < k; i += 32) xs[i * ldsm + c] = fma(-tw, xs[i * ldsm + j], xs[i * ldsm + c]);
-      }
-      __syncthreads();
-    }
-    for (int i = j + 1 + tid; i < k; i += QT) xs[i * ldsm + j] *= -tau;
-    if (tid == 0) xs[j * ldsm + j] = 1.0 - tau;
-    for (int i = tid; i < j; i += QT) xs[i * ldsm + j] = 0.0;
-    __syncthreads();
-  }
-  for (int e = tid; e < k * n; e += QT) {
-    const int i = e / n, c = e % n;
-    X[(r0 + i) * ldx + c] = c < kmax ? xs[i * ldsm + c] : 0.0;
+  for (int q = 0; q < RPT; ++q) {
+    const int i = 4 * q + g;
+    row[4 * q] = present ? (i > col ? x[q] : (i == col ? 1.0 : 0.0)) : 0.0;
   }
 }
 
-// Q_block (k x n, ld ldx) <- Q_block * Qup[blk*n .. blk*n + kmax, :] (kmax x n, ld ldu), one CTA per
-// block, Qup's slice staged in shared memory, one thread per (row, column) output in fixed order.
+// W = V^T x over my rows, reduced over the column's 4 lanes
+template <int RPT>
+__device__ __forceinline__ void pan_dots(const double (&x)[RPT], int g, unsigned mask4, const double* vp,
+                                         double (&w)[4]) {
+  const double* row = vp + (size_t)g * (RPT * 4 + 4);
+  w[0] = w[1] = w[2] = w[3] = 0.0;
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const double2 a = *reinterpret_cast<const double2*>(row + 4 * q);
+    const double2 b = *reinterpret_cast<const double2*>(row + 4 * q + 2);
+    w[0] = fma(a.x, x[q], w[0]);
+    w[1] = fma(a.y, x[q], w[1]);
+    w[2] = fma(b.x, x[q], w[2]);
+    w[3] = fma(b.y, x[q], w[3]);
+  }
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    w[h] += __shfl_xor_sync(mask4, w[h], 1);
+    w[h] += __shfl_xor_sync(mask4, w[h], 2);
+  }
+}
+
+// x -= V w
+template <int RPT>
+__device__ __forceinline__ void pan_update(double (&x)[RPT], int g, const double* vp, const double (&w)[4]) {
+  const volatile double* row = vp + (size_t)g * (RPT * 4 + 4);  // re-read (keeps V out of the registers)
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    double acc = x[q];
+    acc = fma(-row[4 * q], w[0], acc);
+    acc = fma(-row[4 * q + 1], w[1], acc);
+    acc = fma(-row[4 * q + 2], w[2], acc);
+    acc = fma(-row[4 * q + 3], w[3], acc);
+    x[q] = acc;
+  }
+}
+
+template <int RPT, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) k_leaf_qr(double* X, int64_t ldx, int64_t rows, int n, double* R) {
+  constexpr int B = 4 * RPT;
+  __shared__ __align__(16) double vpan[2][4 * (RPT * 4 + 4)];  // group g at g (4 RPT + 4): conflict-free
+  __shared__ double sT[32][16];  // T of panel P: sT[P][4 i + j] = T(i, j)
+  constexpr int PLD = B + 4;  // column stride of the staged panel (bank-conflict-free columns)
+  __shared__ __align__(16) double pan[4 * PLD];  // the panel being factored, column-major
+  __shared__ double xpark[32 * RPT];              // the panel warp's other columns, parked
+  const int t = threadIdx.x, g = t & 3, c = t >> 2, kk = c & 3, P = c >> 2;
+  const int lane = t & 31, lane0 = lane & ~3;
+  const unsigned mask4 = 0xFu << lane0;
+  const unsigned maskP = 0xFFFFu << (lane & 16);
+  const int64_t r0 = (int64_t)blockIdx.x * B;
+  const int k = (int)min((int64_t)B, rows - r0);
+  const int kmax = min(k, n);
+  const bool act = c < n;
+  double x[RPT];
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int i = 4 * q + g;
+    x[q] = (act && i < k) ? X[(r0 + i) * ldx + c] : 0.0;
+  }
+  if (kmax <= 0) return;
+  const int npan = (kmax + 3) / 4;
+  // ---- QR
+  for (int P0 = 0; P0 < npan; ++P0) {
+    const int p = 4 * P0;
+    double* vp = vpan[P0 & 1];
+    double* T = sT[P0];
+    if ((t >> 5) == (P0 >> 1)) {  // the warp holding the panel: factor it in shared memory
+      // its half-warp stages the 4 columns (pan[kk PLD + i]); the other half parks its columns, so
+      // no resident row stays live in registers across the panel code (which would spill)
+      if (P == P0) {
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) pan[kk * PLD + 4 * q + g] = x[q];
+      } else {
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) xpark[q * 32 + lane] = x[q];
+      }
+      __syncwarp();
+      constexpr int RL = B / 32;  // rows per lane: i = lane + 32 r
+      for (int kq = 0; kq < 4; ++kq) {
+        const int col = p + kq;
+        if (col >= kmax) {  // absent reflector: H = I (tau 0, zero column of T)
+          if (lane == 0)
+            for (int i2 = 0; i2 < 4; ++i2) T[4 * i2 + kq] = 0.0;
+          continue;
+        }
+        // (1) dlarfg on rows >= col of column kq: sum of squares below the diagonal, one reduction
+        double val[RL];
+        double sq = 0.0;
+#pragma unroll
+        for (int r = 0; r < RL; ++r) {
+          const int i = lane + 32 * r;
+          val[r] = pan[kq * PLD + i];
+          sq = fma(i > col ? val[r] : 0.0, val[r], sq);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        const double alpha = pan[kq * PLD + col];
+        double tau = 0.0, scale = 0.0, beta = alpha;
+        if (sq > 0.0) {
+          const double nrm = sqrt(fma(alpha, alpha, sq));
+          beta = alpha >= 0.0 ? -nrm : nrm;
+          tau = (beta - alpha) / beta;
+          scale = 1.0 / (alpha - beta);
+        }
+        // (2) v (unit at col, zero above) and, in ONE fused reduction of three values: the dots
+        //     d_k2 = v^T u_k2 of the panel's later columns (k2 > kq) and z_i2 = v_i2^T v of its
+        //     earlier reflectors (i2 < kq) for T
+        double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int r = 0; r < RL; ++r) {
+          const int i = lane + 32 * r;
+          const double v = i > col ? val[r] * scale : (i == col ? 1.0 : 0.0);
+          val[r] = v;
+          const double u[4] = {pan[i], pan[PLD + i], pan[2 * PLD + i], pan[3 * PLD + i]};
+#pragma unroll
+          for (int k2 = 0; k2 < 4; ++k2) {
+            if (k2 == kq) continue;
+            // slot: later columns k2 > kq use acc[k2 - 1 - ... ]; simpler: acc index = k2 < kq ? k2 : k2 - 1
+            const int slot = k2 < kq ? k2 : k2 - 1;
+            // earlier reflector i2 = k2 < kq: v_i2 = u (i > p + k2), 1 (i == p + k2), 0 above
+            const double w = k2 < kq ? (i > p + k2 ? u[k2] : (i == p + k2 ? 1.0 : 0.0)) : u[k2];
+            acc[slot] = fma(v, w, acc[slot]);
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 3; ++h)
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) acc[h] += __shfl_xor_sync(0xffffffffu, acc[h], o);
+        __syncwarp();  // every lane has read the panel before it is rewritten
+        // (3) write v into column kq (beta on the diagonal), apply H to the later columns:
+        //     u_k2 -= tau d_k2 v  (rows >= col)
+#pragma unroll
+        for (int r = 0; r < RL; ++r) {
+          const int i = lane + 32 * r;
+          if (i < col) continue;
+          pan[kq * PLD + i] = i == col ? beta : val[r];
+#pragma unroll
+          for (int k2 = 0; k2 < 4; ++k2)
+            if (k2 > kq) pan[k2 * PLD + i] = fma(-tau * acc[k2 - 1], val[r], pan[k2 * PLD + i]);
+        }
+        // (4) column kq of T (dlarft): T(0:kq, kq) = -tau T(0:kq, 0:kq) z, T(kq, kq) = tau
+        if (lane == 0) {
+          T[5 * kq] = tau;
+#pragma unroll
+          for (int i2 = 0; i2 < 3; ++i2) {
+            if (i2 < kq) {
+              double s2 = 0.0;
+#pragma unroll
+              for (int j2 = 0; j2 < 3; ++j2)
+                if (j2 >= i2 && j2 < kq) s2 = fma(T[4 * i2 + j2], acc[j2], s2);
+              T[4 * i2 + kq] = -tau * s2;
+            }
+          }
+          for (int i2 = kq + 1; i2 < 4; ++i2) T[4 * i2 + kq] = 0.0;
+        }
+        __syncwarp();
+      }
+      // publish V for the trailing update: vp[(g RPT + q) 4 + k] = v_k(row 4q + g)
+#pragma unroll
+      for (int r = 0; r < RL; ++r) {
+        const int i = lane + 32 * r;
+        double v4[4];
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) {
+          const int c2 = p + k2;
+          v4[k2] = c2 >= kmax ? 0.0 : (i > c2 ? pan[k2 * PLD + i] : (i == c2 ? 1.0 : 0.0));
+        }
+        double* dst = vp + (size_t)(i & 3) * (RPT * 4 + 4) + (i >> 2) * 4;
+        *reinterpret_cast<double2*>(dst) = make_double2(v4[0], v4[1]);
+        *reinterpret_cast<double2*>(dst + 2) = make_double2(v4[2], v4[3]);
+      }
+      __syncwarp();
+      if (P == P0) {  // the panel's columns back: R above / on the diagonal, v below
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) x[q] = pan[kk * PLD + 4 * q + g];
+      } else {
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) x[q] = xpark[q * 32 + lane];
+      }
+    }
+    __syncthreads();
+    if (act && c >= p + 4) {  // C <- (I - V T^T V^T) C
+      double w[4];
+      pan_dots<RPT>(x, g, mask4, vp, w);
+      double u[4];
+      u[0] = T[0] * w[0];
+      u[1] = fma(T[1], w[0], T[5] * w[1]);
+      u[2] = fma(T[2], w[0], fma(T[6], w[1], T[10] * w[2]));
+      u[3] = fma(T[3], w[0], fma(T[7], w[1], fma(T[11], w[2], T[15] * w[3])));
+      pan_update<RPT>(x, g, vp, u);
+    }
+  }
+  // ---- R out (upper triangle; zeros below)
+  if (act) {
+    double* Rb = R + (size_t)blockIdx.x * n * n;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int i = 4 * q + g;
+      if (i < kmax) Rb[(size_t)i * n + c] = c >= i ? x[q] : 0.0;
+    }
+  }
+  // ---- explicit Q (dorgqr order, panels last to first)
+  __syncthreads();
+  if (P == npan - 1) {
+    pan_publish<RPT>(x, c, c < kmax, g, kk, vpan[(npan - 1) & 1]);
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) x[q] = (4 * q + g == c) ? 1.0 : 0.0;
+  }
+  for (int P0 = npan - 1; P0 >= 0; --P0) {
+    __syncthreads();
+    const double* vp = vpan[P0 & 1];
+    const double* T = sT[P0];
+    if (act && c >= 4 * P0 && c < kmax) {  // C <- (I - V T V^T) C
+      double w[4];
+      pan_dots<RPT>(x, g, mask4, vp, w);
+      double u[4];
+      u[0] = fma(T[0], w[0], fma(T[1], w[1], fma(T[2], w[2], T[3] * w[3])));
+      u[1] = fma(T[5], w[1], fma(T[6], w[2], T[7] * w[3]));
+      u[2] = fma(T[10], w[2], T[11] * w[3]);
+      u[3] = T[15] * w[3];
+      pan_update<RPT>(x, g, vp, u);
+    } else if (P == P0 - 1) {  // the next panel publishes its V and resets its columns to e_c
+      pan_publish<RPT>(x, c, c < kmax, g, kk, vpan[(P0 - 1) & 1]);
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) x[q] = (4 * q + g == c) ? 1.0 : 0.0;
+    }
+  }
+  if (act) {
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+      const int i = 4 * q + g;
+      if (i < k) X[(r0 + i) * ldx + c] = c < kmax ? x[q] : 0.0;
+    }
+  }
+}
+
+// Q_block (k x n, ld ldx) <- Q_block * Qup[blk*n .. blk*n + kmax, :] (kmax x n, ld ldu).  One CTA
+// per block: Qup's slice in shared memory, the block in chunks of 32 rows (staged, then
+// overwritten); each thread a 4 x 4 output tile, k-loop in fixed order.
+static constexpr int BM_ROWS = 32;
 __global__ void __launch_bounds__(256) k_block_mul(double* X, int64_t ldx, int64_t rows, int n, int b,
                                                    const double* Qup, int64_t ldu) {
-  extern __shared__ double qs[];  // [n][n]
+  extern __shared__ double sm[];
+  const int ldq = ((n + 3) & ~3);  // Qup rows padded to whole 4-column tiles (zeros)
+  double* qs = sm;                              // [n][ldq]
+  double* xs = sm + (size_t)n * ldq;            // [BM_ROWS][n + 1]
+  const int ldx_s = n + 1;
   const int64_t r0 = (int64_t)blockIdx.x * b;
   const int k = (int)min((int64_t)b, rows - r0);
   const int kmax = min(k, n);
   const double* qu = Qup + (size_t)blockIdx.x * n * ldu;
-  for (int e = threadIdx.x; e < kmax * n; e += blockDim.x) qs[e] = qu[(size_t)(e / n) * ldu + e % n];
-  __syncthreads();
-  // row by row: the row's kmax values to registers through a shared row buffer
-  double* rowbuf = qs + (size_t)n * n;  // [8][n]
-  const int sub = threadIdx.x / 32, lane = threadIdx.x % 32;
-  for (int i0 = 0; i0 < k; i0 += 8) {
-    const int i = i0 + sub;
-    if (i < k)
-      for (int c = lane; c < kmax; c += 32) rowbuf[sub * n + c] = X[(r0 + i) * ldx + c];
-    __syncwarp();
-    if (i < k)
-      for (int c = lane; c < n; c += 32) {
-        double s = 0.0;
-        for (int t = 0; t < kmax; ++t) s = fma(rowbuf[sub * n + t], qs[t * n + c], s);
-        X[(r0 + i) * ldx + c] = s;
+  for (int e = threadIdx.x; e < n * ldq; e += blockDim.x) {
+    const int i = e / ldq, cc = e % ldq;
+    qs[e] = (i < kmax && cc < n) ? qu[(size_t)i * ldu + cc] : 0.0;
+  }
+  const int ncg = ldq / 4;                 // column tiles
+  const int tr = threadIdx.x / ncg, tc = threadIdx.x % ncg;  // tr < 8 (rows 4 tr .. 4 tr + 3)
+  const bool worker = threadIdx.x < 8 * ncg;
+  for (int i0 = 0; i0 < k; i0 += BM_ROWS) {
+    const int nr = min(BM_ROWS, k - i0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nr * kmax; e += blockDim.x) {
+      const int i = e / kmax, cc = e % kmax;
+      xs[i * ldx_s + cc] = X[(r0 + i0 + i) * ldx + cc];
+    }
+    __syncthreads();
+    if (worker && 4 * tr < nr) {
+      double acc[4][4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) acc[a][bb] = 0.0;
+      const double* xr = xs + (4 * tr) * ldx_s;
+      const double* qc = qs + 4 * tc;
+      for (int tt = 0; tt < kmax; ++tt) {
+        double av[4], bv[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) av[a] = xr[a * ldx_s + tt];
+        const double2 b01 = *reinterpret_cast<const double2*>(qc + (size_t)tt * ldq);
+        const double2 b23 = *reinterpret_cast<const double2*>(qc + (size_t)tt * ldq + 2);
+        bv[0] = b01.x, bv[1] = b01.y, bv[2] = b23.x, bv[3] = b23.y;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int bb = 0; bb < 4; ++bb) acc[a][bb] = fma(av[a], bv[bb], acc[a][bb]);
       }
-    __syncwarp();
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int i = 4 * tr + a;
+        if (i < nr)
+#pragma unroll
+          for (int bb = 0; bb < 4; ++bb) {
+            const int cc = 4 * tc + bb;
+            if (cc < n) X[(r0 + i0 + i) * ldx + cc] = acc[a][bb];
+          }
+      }
+    }
   }
 }
 
@@ -309,11 +513,9 @@ __global__ void __launch_bounds__(128) k_tsqr_out(const double* svo, int w, cons
 }
 
 // ------------------------------------------------------------- launchers ----
-int tsqr_block_rows(int n) {
-  int b = (24576 / (n + 1)) / 8 * 8;
-  b = b < 256 ? b : 256;
-  return b > n ? b : ((n + 7) / 8) * 8;
-}
+// rows per thread of the leaf kernel: the block is B = 4 RPT rows (>= n), held in registers
+static inline int leaf_rpt(int n) { return n <= 64 ? 64 : 48; }
+int tsqr_block_rows(int n) { return 4 * leaf_rpt(n); }
 
 size_t tsqr_workspace_doubles(int64_t rows, int n) {
   const int b = tsqr_block_rows(n);
@@ -339,30 +541,34 @@ cudaError_t launch_mix_matrix(const double* phases, const int* perms, int ldp, c
 // min(rows, n) zero), R (n x n, upper, row-major ld n; rows past min(rows, n) zero) to R_out.
 // Recursive over levels: leaf QRs of b-row blocks, R stack factored the same way (its own Q),
 // X's blocks multiplied by their rows of that Q.  work: tsqr_workspace_doubles(rows, n).
+static cudaError_t leaf(double* X, int64_t ldx, int64_t rows, int n, double* R, cudaStream_t s) {
+  const int64_t nb = ceil_div(rows, tsqr_block_rows(n));
+  const int threads = 4 * ((n + 7) & ~7);
+  if (leaf_rpt(n) == 64) k_leaf_qr<64, 256><<<(unsigned)nb, threads, 0, s>>>(X, ldx, rows, n, R);
+  else k_leaf_qr<48, 512><<<(unsigned)nb, threads, 0, s>>>(X, ldx, rows, n, R);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_tsqr(double* X, int64_t ldx, int64_t rows, int n, double* R_out, double* work, cudaStream_t s) {
   if (n < 1 || n > 128) return cudaErrorInvalidValue;
   const int b = tsqr_block_rows(n);
-  const size_t smem = (size_t)b * (n + 1) * 8;
-  cudaError_t e = cudaFuncSetAttribute(k_leaf_qr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  cudaError_t e;
   if (rows <= b) {  // one block: R straight out (kmax rows), zero rows below
     e = cudaMemsetAsync(R_out, 0, (size_t)n * n * 8, s);
     if (e != cudaSuccess) return e;
-    k_leaf_qr<<<1, QT, smem, s>>>(X, ldx, rows, n, b, R_out);
-    return cudaGetLastError();
+    return rows > 0 ? leaf(X, ldx, rows, n, R_out, s) : cudaSuccess;
   }
   const int64_t nb = ceil_div(rows, b);
   const int64_t last_k = std::min<int64_t>(n, rows - (nb - 1) * b);
   const int64_t srows = (nb - 1) * n + last_k;  // stacked R rows
   double* Rs = work;  // nb x (n x n): block q's rows at q*n (== the stacking order)
-  k_leaf_qr<<<(unsigned)nb, QT, smem, s>>>(X, ldx, rows, n, b, Rs);
-  e = cudaGetLastError();
+  e = leaf(X, ldx, rows, n, Rs, s);
   if (e != cudaSuccess) return e;
   // the stacked R's: rows [q*n, q*n + kmax_q) of Rs (ld n) -- contiguous because every block
   // but the last has kmax = n
   e = launch_tsqr(Rs, n, srows, n, R_out, work + (size_t)nb * n * n, s);
   if (e != cudaSuccess) return e;
-  const size_t msmem = ((size_t)n * n + 8 * n) * 8;
+  const size_t msmem = ((size_t)n * ((n + 3) & ~3) + (size_t)BM_ROWS * (n + 1)) * 8;
   e = cudaFuncSetAttribute(k_block_mul, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem);
   if (e != cudaSuccess) return e;
   k_block_mul<<<(unsigned)nb, 256, msmem, s>>>(X, ldx, rows, n, b, Rs, n);

@@ -53,11 +53,13 @@ def run(a, passes, seed=1, wp=1e-11):
 # 1e-13 after either algorithm, columns within uv_const eps (sigma_1 / sigma_j)^2 (the Q11 form,
 # loose here).
 @pytest.mark.parametrize("passes", [1, 2])
-@pytest.mark.parametrize("m,n", [(1, 1), (2, 2), (37, 10), (240, 100), (241, 100), (481, 100), (5000, 26),
+@pytest.mark.parametrize("m,n", [(1, 1), (2, 2), (37, 10), (192, 100), (193, 100), (385, 100), (5000, 26),
+                                 (256, 64), (257, 64), (65, 65), (300_001, 66),
                                  (12_345, 33), (100_003, 100), (70_001, 128), (50_000, 127), (3, 3)])
 def test_tsqr_svd_random(m, n, passes):
-    """Several leaf blocks and tree levels with ragged tails (the leaf block of n = 100 is 240
-    rows: 241 leaves a one-row block), odd widths (reading R17), a single row."""
+    """Several leaf blocks and tree levels with ragged tails (the leaf block is 192 rows for
+    n > 64, 256 for n <= 64: 193 / 257 leave a one-row block), odd widths (reading R17), a single
+    row, both leaf shapes around n = 64."""
     rng = np.random.default_rng(m * 7 + n)
     a = rng.standard_normal((m, n)) * np.exp(-np.arange(n) / max(n, 1) * 6)[None, :]
     gpu, ref = run(a, passes)
@@ -113,7 +115,7 @@ def test_tsqr_svd_degenerate():
 def test_tsqr_svd_inplace_and_stats():
     """U may overwrite A (same buffer); the call reports its TSQR passes."""
     rng = np.random.default_rng(9)
-    a = rng.standard_normal((20_000, 50))
+    a = rng.standard_normal((20_000, 50)) * np.exp(-np.arange(50) / 50 * 6)[None, :]
     ph, pm, dph, dpm = draws(50, 4)
     A = to_dev(a)
     u, s, v = tk.tsqr_svd(A, dph, dpm, passes=2, inplace=True)
