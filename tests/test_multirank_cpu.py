@@ -44,10 +44,11 @@ def free_port():
 class Replay:
     """Interprets the orchestrator's trace on one rank (numpy + gloo)."""
 
-    def __init__(self, a_local, omega=None):
+    def __init__(self, a_local, omega=None, mixes=None):
         import oracle
 
         self.o = oracle
+        self.mixes = mixes      # width -> (phases, perms): the draws of Alg. 1/2's Omega
         self.a = a_local
         self.omega = omega
         self.collectives = []   # (what, count) as announced by the trace
@@ -90,16 +91,73 @@ class Replay:
         else:
             raise AssertionError(f"unknown collective {what}")
 
+    # -- Alg. 1 / 2 tokens (TSQR cores)
+    def run_tsqr(self, tok):
+        o = self.o
+        parts = tok.split(":")
+        k = parts[0]
+        c = getattr(self, "c", {})
+        if k == "tsqr_core":
+            self.mode = "tsqr"
+            self.dist = parts[1] == "sharded"
+            self.passes = int(parts[2])
+            self.x = self.cur if self.cur is not None else self.a
+            self.c = {"R": []}
+        elif k == "mix":  # B^* = every row mixed (the draws for this factorization's width)
+            ph, pm = self.mixes(self.x.shape[1])
+            c["ph"], c["pm"] = ph, pm
+            c["q"] = o.mix_rows(self.x, ph, pm)
+        elif k == "tsqr":  # the rank's local QR (the top of the tree follows if sharded)
+            q, r = np.linalg.qr(c["q"], mode="reduced")
+            c["q"], c["r"] = q, r
+            if not self.dist:
+                c["R"].append(r)
+        elif k == "allgather":  # R_p of every rank, stacked in rank order, factored again
+            w = c["r"].shape[1]
+            count = int(parts[2])
+            assert count >= w * w, (count, w)
+            self.collectives.append(("allgather", count))
+            rl = np.zeros((w, w))
+            rl[:c["r"].shape[0]] = c["r"]
+            bufs = [torch.zeros((w, w), dtype=torch.float64) for _ in range(dist.get_world_size())]
+            dist.all_gather(bufs, torch.from_numpy(rl))
+            stack = np.vstack([b.numpy() for b in bufs])
+            qt, r = np.linalg.qr(stack, mode="reduced")
+            rank = dist.get_rank()
+            qloc = np.zeros((c["q"].shape[0], w))
+            qloc[:, :c["q"].shape[1]] = c["q"]
+            c["q"] = qloc @ qt[rank * w:(rank + 1) * w]
+            c["R"].append(r)
+        elif k == "discard":  # |R_jj| < |R_11| wp (reading R18); rows of R, columns of Q
+            r = c["R"][-1]
+            keep = o.r_keep(r, WP)
+            c["q"], c["R"][-1] = c["q"][:, keep], r[keep, :]
+        elif k == "zero_cols":  # Alg. 2: the kept Q~ is QR'd again
+            pass
+        elif k == "svd":
+            mat = c["R"][0] if self.passes == 1 else c["R"][1] @ c["R"][0]
+            ut, sig, vth = np.linalg.svd(mat, full_matrices=False)
+            c["ut"], c["sig"], c["vth"] = ut, sig, vth
+        elif k == "tsqr_out":
+            c["U"], c["S"] = c["q"] @ c["ut"], c["sig"]
+            c["V"] = o.mix_rows(c["vth"], c["ph"], c["pm"], inverse=True).T
+        else:
+            raise AssertionError(f"unknown tsqr token {tok}")
+
     # -- one token
     def run(self, tok):
         o = self.o
         parts = tok.split(":")
         k = parts[0]
-        if k in ("tssvd", "lowrank", "finish", "sync", "build_z", "h2d", "d2h"):
+        if k in ("tssvd", "lowrank", "finish", "sync", "build_z", "h2d", "d2h", "tsqr_svd", "tsqr_top"):
             return
+        if k == "tsqr_core" or getattr(self, "mode", "") == "tsqr" and k in (
+                "mix", "tsqr", "allgather", "discard", "zero_cols", "svd", "tsqr_out"):
+            return self.run_tsqr(tok)
         if k == "allreduce":
             self.allreduce(parts[1], int(parts[2]))
         elif k == "core":
+            self.mode = "gram"
             self.dist = parts[1] == "sharded"
             self.passes = int(parts[2])
             self.x = self.cur if self.cur is not None else self.a
@@ -165,23 +223,26 @@ class Replay:
             raise AssertionError(f"unknown trace token {tok}")
 
 
+MIX_SEED = 5
+
+
 def _replay(rank, world, problem, name, m, n, trace):
     import synth
     from paper_1612_08709_b200 import shard_rows
 
-    if problem == "tssvd":
+    if problem in ("tssvd", "tsqr"):
         d = synth.config_inputs(name, m=m)
         omega = None
     else:
         d = synth.config_inputs(name, m=m, n=n)
         omega = d["Omega"]
     r0, r1 = shard_rows(d["A"].shape[0], world, rank)
-    rp = Replay(d["A"][r0:r1], omega)
+    rp = Replay(d["A"][r0:r1], omega, lambda w: synth.mixing_params(w, MIX_SEED))
     rp.qt = None
     rp.k = d.get("k", 0)
     for tok in trace:
         rp.run(tok)
-    if problem == "tssvd":
+    if problem in ("tssvd", "tsqr"):
         res = (rp.out["U"], rp.out["S"], rp.out["V"])
     else:
         res = rp.result
@@ -200,10 +261,10 @@ def _worker(rank, world, port, problem, name, m, n, out_q):
         cfg = synth.CONFIGS[name]
         mm = m or cfg["m"]
         r0, r1 = shard_rows(mm, world, rank)
-        if problem == "tssvd":
-            trace = _lib.trace("tssvd", world, r1 - r0, n or cfg["n"], wp=WP)
+        if problem in ("tssvd", "tsqr"):
+            trace = _lib.trace(problem, world, r1 - r0, n or cfg["n"], wp=WP)
         else:
-            trace = _lib.trace("lowrank", world, r1 - r0, n, cfg["l"], cfg["iters"], cfg["k"], wp=WP)
+            trace = _lib.trace(problem, world, r1 - r0, n, cfg["l"], cfg["iters"], cfg["k"], wp=WP)
         (u, s, v), coll = _replay(rank, world, problem, name, m, n, trace)
         g = torch.from_numpy(np.ascontiguousarray(u.T @ u))
         dist.all_reduce(g)  # orthonormality of the distributed U
@@ -270,6 +331,51 @@ def test_two_rank_lowrank_trace_replay():
     assert o0 <= 1e-13
     d = synth.config_inputs("c3", m=m, n=n)
     ref = oracle.lowrank_svd(d["A"], d["Omega"], cfg["iters"], cfg["k"], WP)
+    assert s0.size == ref[1].size == cfg["k"]
+    assert_lowrank_parity((np.vstack([u0, u1]), s0, v0), ref, d["A"], d["x0"])
+
+
+@pytest.mark.parametrize("name,m", [("c2", 60_000), ("c1", None)])
+def test_two_rank_tsqr_trace_replay(name, m):
+    """tsqr_svd (Alg. 2) on 2 ranks from the orchestrator's trace: each rank's local QR, the R
+    factors all-gathered (rank order) and factored again identically, Q_p times its rows of that
+    factor (the top of the TSQR tree), discards and the SVD of T = R R~ replicated; no host round
+    trip before the end; the single-process oracle (same Omega draws) reproduced."""
+    import oracle
+    import synth
+
+    res = _run_world("tsqr", name, m)
+    (_, t0, c0, s0, v0, u0, o0), (_, t1, c1, s1, v1, u1, o1) = res
+    assert t0 == t1 and _syncs(t0) == [] and t0[-1] == "finish"
+    n = synth.CONFIGS[name]["n"]
+    assert [w for w, _ in c0] == ["m", "allgather", "allgather"]
+    assert all(cnt == n * n for w, cnt in c0 if w == "allgather")
+    assert np.array_equal(s0, s1) and np.array_equal(v0, v1)
+    assert o0 <= 1e-13
+    d = synth.config_inputs(name, m=m)
+    ref = oracle.tsqr_svd(d["A"], *synth.mixing_params(n, MIX_SEED), WP, 2)
+    assert_tssvd_parity((np.vstack([u0, u1]), s0, v0), ref, passes=2, sigma_tol=1e-13)
+
+
+def test_two_rank_lowrank_tsqr_trace_replay():
+    """lowrank_svd_tsqr (Alg. 7) on 2 ranks from the trace: TSQR cores with the R all-gather for
+    the row-sharded factors, local TSQR for the replicated n x l ones, the A^T Q allreduce;
+    one round trip; the single-process oracle reproduced."""
+    import oracle
+    import synth
+
+    m, n = 8_000, 1_001
+    res = _run_world("lowrank_tsqr", "c3", m, n)
+    (_, t0, c0, s0, v0, u0, o0), (_, t1, c1, s1, v1, u1, o1) = res
+    assert t0 == t1 and _syncs(t0) == [] and t0[-1] == "finish"
+    cfg = synth.CONFIGS["c3"]
+    whats = [w for w, _ in c0]
+    assert whats.count("allgather") == cfg["iters"] + 2 and whats.count("beta") == cfg["iters"] + 1
+    assert np.array_equal(s0, s1) and np.array_equal(v0, v1)
+    assert o0 <= 1e-13
+    d = synth.config_inputs("c3", m=m, n=n)
+    ref = oracle.lowrank_svd_tsqr(d["A"], d["Omega"], cfg["iters"], cfg["k"],
+                                  lambda w: synth.mixing_params(w, MIX_SEED), WP)
     assert s0.size == ref[1].size == cfg["k"]
     assert_lowrank_parity((np.vstack([u0, u1]), s0, v0), ref, d["A"], d["x0"])
 
