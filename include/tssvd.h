@@ -194,6 +194,22 @@ int lowrank_svd_tsqr(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n,
                      double* sigma, double* V, int64_t ldv, int64_t* rank, void* workspace,
                      size_t workspace_bytes);
 
+/* ---- problem {2}, Algorithm 8 with LU-based subspace tracking ---
+ * lowrank_svd() with Alg. 5's intermediate steps 4 and 6 taking the L factor of Gaussian
+ * elimination with partial (row) pivoting of Y_j / Y~_j instead of Alg. 3's orthonormal Q ("the
+ * column space of L is the same as the column space of Q"); the last step (Alg. 4) and Alg. 6
+ * unchanged.  Pivots: the largest |.| among the rows not yet chosen, ties to the lowest global
+ * row (rank order); elimination stops at the first pivot with |pivot_j| <= |pivot_1| wp.  Every
+ * pivot decision stays on the device (multi-rank: three small allreduces per column).  Arguments,
+ * outputs and errors as lowrank_svd() (host_io 0 and 1).
+ */
+int lowrank_lu_workspace_size(const tssvd_comm* comm, int64_t m_local, int64_t n, int64_t l,
+                              const tssvd_opts* opts, size_t* bytes);
+int lowrank_svd_lu(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, const double* A,
+                   int64_t lda, const double* Omega, int64_t ldo, int64_t l, int iters, int64_t k,
+                   const tssvd_opts* opts, double* U, int64_t ldu, double* sigma, double* V,
+                   int64_t ldv, int64_t* rank, void* workspace, size_t workspace_bytes);
+
 /* ---- instrumentation ------------------------------------------------------
  * Per-call counters of the last tssvd()/lowrank_svd() on this thread:
  * kernel launches enqueued, Jacobi sweeps of each core, and the kept ranks. */
@@ -255,7 +271,8 @@ int tssvd_sym_eig(void* stream, int64_t n, const double* B, int64_t ldb, double*
 size_t tssvd_sym_eig_workspace(int64_t n);
 
 /* Plan-only run (no GPU, no CUDA or NCCL call): the steps and collectives that
- * tssvd() (problem = 1; l, iters, k ignored) or lowrank_svd() (problem = 2) would
+ * tssvd() (problem = 1; l, iters, k ignored), lowrank_svd() (2), tsqr_svd() (3),
+ * lowrank_svd_tsqr() (4) or lowrank_svd_lu() (5) would
  * take on one of `nranks` ranks holding m_local rows, written to buf as
  * "token;token;..." (e.g. "gram:X;allreduce:gram:5050;eig:B;...").  Used by the
  * multi-rank CPU tests, whose replay of the distributed data flow is driven by

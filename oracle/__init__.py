@@ -21,6 +21,8 @@ from .gram_svd import (  # noqa: F401
     gram,
     keep_mask,
     lowrank_svd,
+    lowrank_svd_lu,
+    lu_tracking_factor,
     lowrank_svd_tsqr,
     mix_rows,
     r_keep,

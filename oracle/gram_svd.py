@@ -26,6 +26,8 @@ Readings of the paper taken here (all listed in DESIGN.md "Readings"):
   R5 signs: each (u_j, v_j) flipped so the largest-|.| entry of v_j is positive.
   R6 Alg. 6's SVD of B = Q^T A (l x n) is Alg. 4 applied to B^T (n x l).
   R7 Alg. 8 returns the leading k <= l triplets.
+  R21 LU-based tracking: partial row pivoting, stop at the first pivot with
+      |pivot_j| <= |pivot_1| wp.
 """
 from __future__ import annotations
 
@@ -380,3 +382,62 @@ def lowrank_svd_tsqr(a: np.ndarray, omega: np.ndarray, i: int, k: int | None, mi
     kk = min(k, sig.size)
     u, v = canonical_signs(u[:, :kk], v[:, :kk])
     return u, sig[:kk], v
+
+
+# ---------------------------------------- LU-based subspace tracking --
+def lu_tracking_factor(y: np.ndarray, wp: float = DEFAULT_WP):
+    """in the intermediate steps of Alg. 5 'replacing Q with the lower
+    triangular/trapezoidal factor L in an LU factorization is sufficient ... the column space of L
+    is the same as the column space of Q'.  Gaussian elimination with partial (row) pivoting of
+    the tall Y, column by column: the pivot of column j is its largest-|.| entry among the rows
+    not yet chosen (ties: the lowest row index); the multipliers y_ij / pivot form column j of L;
+    the remaining columns lose the multiple of the pivot row.  Returned L is Y's row order (the
+    P L of Y = P L U): 1 at each pivot row's own column, 0 right of it.  Reading R21: elimination
+    stops at the first numerically zero pivot, |pivot_j| <= |pivot_1| wp (the Alg. 1 rule,
+    P:534-538); the r columns before it are returned."""
+    w = np.array(y, dtype=np.float64, copy=True)
+    m, l = w.shape
+    lmat = np.zeros((m, l))
+    chosen = np.zeros(m, dtype=bool)
+    p1 = 0.0
+    r = 0
+    for j in range(l):
+        mag = np.abs(w[:, j])
+        mag[chosen] = -1.0
+        p = int(np.argmax(mag))
+        pv = w[p, j]
+        if j == 0:
+            p1 = abs(pv)
+        if not (p1 > 0.0 and abs(pv) > p1 * wp):
+            break
+        mult = w[:, j] / pv
+        mult[chosen] = 0.0
+        mult[p] = 1.0
+        lmat[:, j] = mult
+        urow = w[p, j + 1:].copy()
+        w[:, j + 1:] -= np.outer(mult, urow)
+        chosen[p] = True
+        r = j + 1
+    return lmat[:, :r], r
+
+
+def lowrank_svd_lu(a: np.ndarray, omega: np.ndarray, i: int, k: int | None = None,
+                   wp: float = DEFAULT_WP):
+    """Alg. 8 with LU-based subspace tracking: Alg. 5's steps 4 and 6
+    take the L factor of Y_j / Y~_j (lu_tracking_factor) instead of Alg. 3's Q; the last step
+    (Alg. 4) and Alg. 6 are unchanged.  The column spaces are those of Alg. 8, so in exact
+    arithmetic the result is Alg. 8's."""
+    l = omega.shape[1]
+    k = l if k is None else k
+    qt = omega
+    for _ in range(i):
+        # Step 3 (P:715), step 4 with L (P:405-409)
+        q, _ = lu_tracking_factor(a @ qt, wp)
+        # Step 5 (P:722), step 6 with L
+        qt, _ = lu_tracking_factor(a.T @ q, wp)
+    # Step 8 (P:731), step 9 (P:733-739): Alg. 4
+    q, _, _ = alg4(a @ qt, wp)
+    u, s, v = direct_svd(a, q, wp)
+    kk = min(k, s.size)
+    u, v = canonical_signs(u[:, :kk], v[:, :kk])
+    return u, s[:kk], v

@@ -75,6 +75,11 @@ SIGNATURES = [
                                  c_int64, c_int64, c_int, c_int64, c_void_p, c_void_p, P(TssvdOpts),
                                  c_void_p, c_int64, c_void_p, c_void_p, c_int64, P(c_int64), c_void_p,
                                  c_size_t]),
+    ("lowrank_lu_workspace_size", c_int, [c_void_p, c_int64, c_int64, c_int64, P(TssvdOpts),
+                                          P(c_size_t)]),
+    ("lowrank_svd_lu", c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p,
+                               c_int64, c_int64, c_int, c_int64, P(TssvdOpts), c_void_p, c_int64,
+                               c_void_p, c_void_p, c_int64, P(c_int64), c_void_p, c_size_t]),
     ("tssvd_last_stats", c_int, [P(TssvdStats)]),
     ("tssvd_set_pass_timing", c_int, [c_int]),
     ("tssvd_gram", c_int, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p, c_int64,
@@ -163,7 +168,7 @@ def trace(problem: str, nranks: int, m_local: int, n: int, l: int = 0, iters: in
     real orchestrator (no GPU needed)."""
     opts = default_opts(wp, passes)
     buf = ctypes.create_string_buffer(1 << 16)
-    code = {"tssvd": 1, "lowrank": 2, "tsqr": 3, "lowrank_tsqr": 4}[problem]
+    code = {"tssvd": 1, "lowrank": 2, "tsqr": 3, "lowrank_tsqr": 4, "lowrank_lu": 5}[problem]
     check(lib().tssvd_trace(code, nranks, m_local, n, l, iters, k, ctypes.byref(opts), buf, len(buf)))
     return [t for t in buf.value.decode().split(";") if t]
 

@@ -138,13 +138,19 @@ def tssvd(A: torch.Tensor, wp: float = 1e-11, passes: int = 2, comm: Comm | None
 
 def lowrank_svd(A: torch.Tensor, Omega: torch.Tensor, iters: int, k: int | None = None,
                 wp: float = 1e-11, comm: Comm | None = None, max_sweeps: int = 60,
-                out_of_core: bool = False):
+                out_of_core: bool = False, tracking: str = "q"):
     """Rank-k approximation U diag(sigma) V^T of the row-sharded A by Algorithm 8.
 
     Omega (n x l) is the Gaussian start block of Alg. 5 step 1 (identical on every rank).
     out_of_core (CPU tensors only): A stays in host memory and every pass over it streams row
     chunks (opts.host_io = 2) -- for A larger than the GPU's memory.
+    tracking="lu": the intermediate steps take the L of an LU factorization with partial
+    pivoting instead of Q (lowrank_svd_lu in the C ABI).
     """
+    if tracking not in ("q", "lu"):
+        raise ValueError("tracking must be 'q' or 'lu'")
+    if tracking == "lu" and out_of_core:
+        raise ValueError("LU tracking is not offered out of core")
     _check_tall(A)
     m, n = A.shape
     l = Omega.shape[1]
@@ -159,7 +165,8 @@ def lowrank_svd(A: torch.Tensor, Omega: torch.Tensor, iters: int, k: int | None 
     opts = default_opts(wp, 2, max_sweeps, host_io=2 if out_of_core else host)
     cptr = comm.ptr if comm else None
     nbytes = ctypes.c_size_t()
-    check(lib().lowrank_workspace_size(cptr, m, n, l, ctypes.byref(opts), ctypes.byref(nbytes)))
+    wsf = lib().lowrank_lu_workspace_size if tracking == "lu" else lib().lowrank_workspace_size
+    check(wsf(cptr, m, n, l, ctypes.byref(opts), ctypes.byref(nbytes)))
     ws = _workspace(nbytes.value, dev)
     pin = host and torch.cuda.is_available()
     kk = max(k, 1)
@@ -168,10 +175,11 @@ def lowrank_svd(A: torch.Tensor, Omega: torch.Tensor, iters: int, k: int | None 
     sigma = torch.empty(kk, dtype=torch.float64, device=A.device, pin_memory=pin)
     V = torch.empty((n, kk), dtype=torch.float64, device=A.device, pin_memory=pin)
     r = ctypes.c_int64()
-    check(lib().lowrank_svd(cptr, _stream(dev), m, n, A.data_ptr(), A.stride(0) if m > 0 else n,
-                            Omega.data_ptr(), Omega.stride(0), l, iters, k, ctypes.byref(opts),
-                            U.data_ptr(), ldu, sigma.data_ptr(), V.data_ptr(), kk, ctypes.byref(r),
-                            ws.data_ptr(), ws.numel()))
+    fn = lib().lowrank_svd_lu if tracking == "lu" else lib().lowrank_svd
+    check(fn(cptr, _stream(dev), m, n, A.data_ptr(), A.stride(0) if m > 0 else n,
+             Omega.data_ptr(), Omega.stride(0), l, iters, k, ctypes.byref(opts),
+             U.data_ptr(), ldu, sigma.data_ptr(), V.data_ptr(), kk, ctypes.byref(r),
+             ws.data_ptr(), ws.numel()))
     q = r.value
     return U[:, :q], sigma[:q], V[:, :q]
 

@@ -1084,10 +1084,55 @@ void tssvd_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, cons
   *rank = r;
 }
 
+// ------------------------------------- LU-based subspace tracking --
+// X (rows x w, ldx; row-sharded when dist) becomes the L of Gaussian elimination with partial
+// pivoting, in place (csrc/lu_track.cu), every decision on the device: per column the rank-local
+// pivot candidate, a MAX allreduce of its magnitude and a MIN allreduce of the owning rank (ties
+// to the lowest rank, then the lowest local row), the pivot row summed across ranks (the owner
+// contributes it, the others zeros), the elimination.  The kept count r (first numerically zero
+// pivot, reading R21) goes to a decision slot; columns >= r are zero.
+CoreOut lu_core(Ctx& c, void* lws, double* X, int64_t ldx, int64_t rows, int w, const int* wdev, bool dist) {
+  cudaStream_t s = c.s;
+  Ctx cd = c;
+  if (!dist) cd.comm = nullptr;
+  const bool dd = cd.dist();
+  step("lu_core:%s:%d", dist ? "sharded" : "local", w);
+  const LuWork lw = lu_carve(lws, rows, w);
+  const int rank = dd ? c.comm->rank : 0;
+  KL(lu_init(lw, rows, s));
+  for (int j = 0; j < w; ++j) {
+    step("lu_col:%d", j);
+    KL(lu_colmax(lw, X, ldx, rows, j, s));
+    if (dd) {
+      step("allreduce:lu_max:1");
+      if (!g_dry) NC(ncclAllReduce(lw.gbuf, lw.gbuf, 1, ncclDouble, ncclMax, c.comm->nccl, s));
+    }
+    KL(lu_owner(lw, rank, s));
+    if (dd) {
+      step("allreduce:lu_owner:1");
+      if (!g_dry) NC(ncclAllReduce(lw.obuf, lw.obuf, 1, ncclInt32, ncclMin, c.comm->nccl, s));
+    }
+    KL(lu_decide(lw, X, ldx, w, j, wdev, c.wp, rank, s));
+    if (dd) {
+      step("allreduce:lu_row:%d", w + 1);
+      if (!g_dry) NC(ncclAllReduce(lw.urow, lw.urow, (size_t)w + 1, ncclDouble, ncclSum, c.comm->nccl, s));
+    }
+    KL(lu_update(lw, X, ldx, rows, w, j, s));
+  }
+  const int sl = c.next_slot();
+  step("lu_finish");
+  KL(lu_finish(lw, X, ldx, rows, w, c.slot(sl), s));
+  CoreOut out;
+  out.bound = w;
+  out.slot = sl;
+  return out;
+}
+
 // ------------------------------------------------------------- low rank --
 struct LrPlan {
   Core tall, small;
   TsqrCore tq_tall, tq_small;  // Alg. 7 (method 1)
+  void *lu_tall, *lu_small;     // LU-based tracking (method 2)
   int* ctl;
   double *Qt, *Y, *Z, *tn, *Ut, *sig_tmp, *v_scr, *sig_scr, *Mfin, *sk;
   double *a_stage, *a_stage2, *o_stage, *u_stage, *s_stage, *vo_stage;
@@ -1099,9 +1144,13 @@ size_t plan_lowrank(Arena& a, LrPlan& p, int64_t m_local, int n, int l, const ts
   p.lp = (l + 1) & ~1;
   p.ldzmax = pad8(l);
   p.ctl = a.get<int>(kCtlInts);
-  if (method == 0) {
+  if (method != 1) {
     p.tall.alloc(a, m_local, l);
     p.small.alloc(a, n, l);
+    if (method == 2) {
+      p.lu_tall = a.get<char>(lu_workspace_bytes(m_local, l));
+      p.lu_small = a.get<char>(lu_workspace_bytes(n, l));
+    }
   } else {
     p.tq_tall.alloc(a, m_local, l, nranks);
     p.tq_small.alloc(a, n, l, 1);
@@ -1215,7 +1264,8 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
                   int64_t ldv, int64_t* rank, void* ws, size_t ws_bytes, int method = 0,
                   const double* mph = nullptr, const int* mpm = nullptr) {
   // method 0: Algorithm 8 (Gram-based cores); 1: Algorithm 7 (TSQR-based cores, the random
-  // mixing draws per width in the tables mph / mpm, ld l)
+  // mixing draws per width in the tables mph / mpm, ld l); 2: Algorithm 8 with LU-based subspace
+  // tracking in the iterations
   g_stats = tssvd_stats{};
   check_opts(opts);
   if (m_local < 0) fail(TSSVD_EINVAL, "m_local < 0");
@@ -1341,8 +1391,13 @@ void lowrank_impl(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, co
   const int* wprev = nullptr;
   auto fact = [&](Core& cb, TsqrCore& tb, double* X, int64_t ldx, int64_t rows, int w, int passes, bool dist,
                   double* sg, double* Vv) -> CoreOut {
-    CoreOut o = method == 0 ? core(c, cb, X, ldx, rows, w, passes, dist, X, ldx, sg, Vv, Lc, true)
-                            : tsqr_core(c, tb, X, ldx, rows, w, wprev, mph, mpm, Lc, passes, dist, X, ldx, sg, Vv, Lc);
+    CoreOut o;
+    if (method == 1)
+      o = tsqr_core(c, tb, X, ldx, rows, w, wprev, mph, mpm, Lc, passes, dist, X, ldx, sg, Vv, Lc);
+    else if (method == 2 && passes == 1)  // Alg. 5 steps 4 / 6: L instead of Q
+      o = lu_core(c, &cb == &p.tall ? p.lu_tall : p.lu_small, X, ldx, rows, w, wprev, dist);
+    else
+      o = core(c, cb, X, ldx, rows, w, passes, dist, X, ldx, sg, Vv, Lc, true);
     wprev = c.slot(o.slot) + kSlotR;
     return o;
   };
@@ -1664,6 +1719,28 @@ int lowrank_tsqr_workspace_size(const tssvd_comm* comm, int64_t m_local, int64_t
   });
 }
 
+int lowrank_lu_workspace_size(const tssvd_comm* comm, int64_t m_local, int64_t n, int64_t l,
+                              const tssvd_opts* opts, size_t* bytes) {
+  return guarded([&] {
+    check_opts(opts);
+    if (m_local < 0 || n < 2 || l < 1 || l > 128 || l >= n) fail(TSSVD_EINVAL, "bad sizes");
+    if (!bytes) fail(TSSVD_EINVAL, "bytes is NULL");
+    Arena a;
+    LrPlan p;
+    *bytes = plan_lowrank(a, p, m_local, (int)n, (int)l, opts, 2, comm ? comm->nranks : 1) + 256;
+  });
+}
+
+int lowrank_svd_lu(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, const double* A, int64_t lda,
+                   const double* Omega, int64_t ldo, int64_t l, int iters, int64_t k, const tssvd_opts* opts,
+                   double* U, int64_t ldu, double* sigma, double* V, int64_t ldv, int64_t* rank, void* workspace,
+                   size_t workspace_bytes) {
+  return guarded([&] {
+    lowrank_impl(comm, stream, m_local, n, A, lda, Omega, ldo, l, iters, k, opts, U, ldu, sigma, V, ldv, rank,
+                 workspace, workspace_bytes, 2);
+  });
+}
+
 int lowrank_svd_tsqr(tssvd_comm* comm, void* stream, int64_t m_local, int64_t n, const double* A,
                      int64_t lda, const double* Omega, int64_t ldo, int64_t l, int iters, int64_t k,
                      const double* phases, const int* perms, const tssvd_opts* opts, double* U, int64_t ldu,
@@ -1685,8 +1762,9 @@ int tssvd_trace(int problem, int nranks, int64_t m_local, int64_t n, int64_t l, 
     ~DryScope() { g_dry = false; }
   };
   return guarded([&] {
-    if (problem < 1 || problem > 4)
-      fail(TSSVD_EINVAL, "problem must be 1 (tssvd), 2 (lowrank_svd), 3 (tsqr_svd) or 4 (lowrank_svd_tsqr)");
+    if (problem < 1 || problem > 5)
+      fail(TSSVD_EINVAL,
+           "problem must be 1 (tssvd), 2 (lowrank_svd), 3 (tsqr_svd), 4 (lowrank_svd_tsqr) or 5 (lowrank_svd_lu)");
     if (nranks < 1 || !buf || buf_len == 0) fail(TSSVD_EINVAL, "bad trace arguments");
     check_opts(opts);
     tssvd_opts o = *opts;
@@ -1711,7 +1789,7 @@ int tssvd_trace(int problem, int nranks, int64_t m_local, int64_t n, int64_t l, 
                   fws_bytes);
       else
         lowrank_impl(fcp, nullptr, m_local, n, fake, ld, fake, l, l, iters, k, &o, fake, lk, fake, fake, k, &rank,
-                     fws, fws_bytes, problem == 4 ? 1 : 0, fake, ifake);
+                     fws, fws_bytes, problem == 4 ? 1 : (problem == 5 ? 2 : 0), fake, ifake);
     }
     if (g_trace.size() + 1 > buf_len) fail(TSSVD_ENOMEM, "trace needs %zu bytes", g_trace.size() + 1);
     std::memcpy(buf, g_trace.c_str(), g_trace.size() + 1);

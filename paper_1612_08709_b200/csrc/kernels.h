@@ -100,4 +100,25 @@ cudaError_t launch_tri_mul(const double* R2, const double* R1, int w, double* T,
 cudaError_t launch_tsqr_out(const double* svo, int w, const double* vals, const double* M0, const int* rr,
                             double* sigma, double* V, int64_t ldv, double* Mg, int ldm, cudaStream_t s);
 
+// ---- LU-based subspace tracking (lu_track.cu) ----
+struct LuWork {
+  void* rec;
+  unsigned char* chosen;
+  double* pval;
+  long long* pidx;
+  double* urow;
+  double* gbuf;  // [0]: the column's max |.| (MAX-allreduced across ranks)
+  double* lbuf;  // [0]: this rank's max
+  int* obuf;     // [0]: owning rank candidate (MIN-allreduced)
+};
+size_t lu_workspace_bytes(int64_t rows, int w);
+LuWork lu_carve(void* ws, int64_t rows, int w);
+cudaError_t lu_init(const LuWork& lw, int64_t rows, cudaStream_t s);
+cudaError_t lu_colmax(const LuWork& lw, const double* Y, int64_t ldy, int64_t rows, int j, cudaStream_t s);
+cudaError_t lu_owner(const LuWork& lw, int rank, cudaStream_t s);
+cudaError_t lu_decide(const LuWork& lw, const double* Y, int64_t ldy, int w, int j, const int* wdev, double wp,
+                      int rank, cudaStream_t s);
+cudaError_t lu_update(const LuWork& lw, double* Y, int64_t ldy, int64_t rows, int w, int j, cudaStream_t s);
+cudaError_t lu_finish(const LuWork& lw, double* Y, int64_t ldy, int64_t rows, int w, int* slot, cudaStream_t s);
+
 }  // namespace tsk

@@ -1,0 +1,117 @@
+"""GPU parity of Alg. 8 with LU-based subspace tracking (lowrank_svd_lu in the C ABI)
+against oracle.lowrank_svd_lu on the same seeded inputs.  Run with `pytest -m gpu` on a B200."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from parity import assert_lowrank_parity
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1612_08709_b200 as tk  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+PAPER = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_values.json")))
+
+
+def to_dev(a):
+    a = np.ascontiguousarray(a)
+    if a.shape[1] & 1:
+        buf = torch.zeros((a.shape[0], a.shape[1] + 1), dtype=torch.float64, device=DEV)
+        buf[:, :a.shape[1]] = torch.from_numpy(a).to(DEV)
+        return buf[:, :a.shape[1]]
+    return torch.from_numpy(a).to(DEV)
+
+
+def run(a, omega, iters, k, host=False):
+    if host:
+        u, s, v = tk.lowrank_svd(torch.from_numpy(np.ascontiguousarray(a)), torch.from_numpy(omega), iters,
+                                 k=k, tracking="lu")
+    else:
+        u, s, v = tk.lowrank_svd(to_dev(a), to_dev(omega), iters, k=k, tracking="lu")
+        torch.cuda.synchronize()
+    return u.cpu().numpy(), s.cpu().numpy(), v.cpu().numpy()
+
+
+@pytest.mark.parametrize("host", [False, True])
+def test_lowrank_lu_c3_scaled(host):
+    """c3's spectrum at 20000 x 2000 (l = 25, i = 2, k = 20): the full low-rank contract against
+    the LU oracle, and against Alg. 8 itself (same column spaces)."""
+    d = synth.config_inputs("c3", m=20_000, n=2_000)
+    gpu = run(d["A"], d["Omega"], d["iters"], d["k"], host)
+    ref = oracle.lowrank_svd_lu(d["A"], d["Omega"], d["iters"], d["k"])
+    assert_lowrank_parity(gpu, ref, d["A"], d["x0"])
+    alg8 = oracle.lowrank_svd(d["A"], d["Omega"], d["iters"], d["k"])
+    assert_lowrank_parity(gpu, alg8, d["A"], d["x0"])
+
+
+@pytest.mark.parametrize("m,n,l,iters,k", [(5_001, 801, 16, 1, 10), (3_000, 1_001, 33, 3, 33), (700, 300, 8, 0, 4)])
+def test_lowrank_lu_shapes(m, n, l, iters, k):
+    """Odd n, l up to 33, i = 0 (no LU at all), i = 3.  The column bound takes uv_const = 1e4: the
+    final Alg. 4 step factors Y = A L~ whose conditioning includes L~'s (not orthonormal), so the
+    Gram-squared rounding of two differently rounded eliminations (GPU FMA updates vs the oracle's
+    separate multiply and subtract; reading R21) differs by up to ~3e3 eps at l = 33, i = 3."""
+    rng = np.random.default_rng(m + n)
+    u0 = np.linalg.qr(rng.standard_normal((m, 40)))[0]
+    v0 = np.linalg.qr(rng.standard_normal((n, 40)))[0]
+    a = (u0 * np.logspace(0, -6, 40)) @ v0.T + 1e-9 * rng.standard_normal((m, n)) / np.sqrt(n)
+    omega = synth.omega(n, l, 3)
+    gpu = run(a, omega, iters, k)
+    ref = oracle.lowrank_svd_lu(a, omega, iters, k)
+    assert_lowrank_parity(gpu, ref, a, synth.power_start(n, 7), uv_const=1e4)
+
+
+def test_lowrank_lu_rank_collapse():
+    """A of exact rank 6 < l = 16: the elimination stops after 6 columns (reading R21), every later
+    factorization has width 6, k = 10 returns the 6 triplets of the oracle."""
+    rng = np.random.default_rng(11)
+    a = rng.standard_normal((4000, 6)) @ rng.standard_normal((6, 300))
+    omega = synth.omega(300, 16, 11)
+    gpu = run(a, omega, 2, 10)
+    ref = oracle.lowrank_svd_lu(a, omega, 2, 10)
+    assert gpu[1].size == ref[1].size == 6
+    assert np.max(np.abs(gpu[1] - ref[1])) <= 1e-12 * ref[1][0]
+
+
+def test_lowrank_lu_table8_matrix():
+    """The paper's Table 8 matrix (Eq. testSl, l = 20, i = 2): sigma_6 / sigma_1 = 5.5e-6 sits 1.7x
+    above the sqrt(wp) discard line; with L instead of Q the final Alg. 4 keeps 5 (oracle and GPU
+    alike: the LU variant loses that borderline direction, R21), residual as the
+    oracle's within 1%."""
+    g = PAPER["alg8_l20_i2_m1e4_n2000"]
+    a, _ = synth.paper_lowrank_test_matrix(g["m"], g["n"], g["l"])
+    om = synth.omega(g["n"], g["l"], 100)
+    gpu = run(a, om, g["i"], g["l"])
+    ref = oracle.lowrank_svd_lu(a, om, g["i"], g["l"])
+    assert gpu[1].size == ref[1].size
+    x0 = synth.power_start(g["n"], 7)
+    eg, er = oracle.spectral_error(a, *gpu, x0), oracle.spectral_error(a, *ref, x0)
+    assert abs(eg - er) <= 0.01 * er
+    assert oracle.ortho_error(gpu[0]) <= 1e-13 and oracle.ortho_error(gpu[2]) <= 1e-13
+
+
+@pytest.mark.slow
+def test_lowrank_lu_c3_full_vs_alg8_gpu():
+    """c3 at full size (200,000 x 20,000, device-built): the LU variant's sigma equals Alg. 8's to
+    1e-10 sigma_1 and both factor sets are orthonormal (no oracle at this size here)."""
+    c = synth.CONFIGS["c3"]
+    d = synth.config_inputs("c3")
+    A = torch.from_numpy(d["A"]).to(DEV)
+    Om = torch.from_numpy(d["Omega"]).to(DEV)
+    u1, s1, v1 = tk.lowrank_svd(A, Om, c["iters"], k=c["k"])
+    u2, s2, v2 = tk.lowrank_svd(A, Om, c["iters"], k=c["k"], tracking="lu")
+    torch.cuda.synchronize()
+    s1, s2 = s1.cpu().numpy(), s2.cpu().numpy()
+    assert s1.size == s2.size == c["k"]
+    assert np.max(np.abs(s1 - s2)) <= 1e-10 * s1[0]
+    for u in (u2, v2):
+        g = (u.T @ u).cpu().numpy()
+        assert np.max(np.abs(g - np.eye(g.shape[0]))) <= 1e-13

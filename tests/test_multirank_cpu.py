@@ -57,8 +57,71 @@ class Replay:
         self.dist = False
         self.out = {}           # outputs of the last finished core
 
+    # -- LU-based tracking: distributed partial pivoting, one column per token
+    def lu_local(self, j):
+        lu = self.lu
+        w = lu["W"]
+        lu["j"] = j
+        if lu["stopped"] or j >= w.shape[1]:
+            lu["val"], lu["idx"] = -1.0, -1
+            return
+        mag = np.abs(w[:, j]) if w.shape[0] else np.zeros(0)
+        if w.shape[0]:
+            mag[lu["chosen"]] = -1.0
+        lu["idx"] = int(np.argmax(mag)) if mag.size else -1
+        lu["val"] = float(mag[lu["idx"]]) if mag.size else -1.0
+
+    def lu_step(self, gmax, owner, urow):
+        lu = self.lu
+        j = lu["j"]
+        w = lu["W"]
+        if lu["stopped"] or j >= w.shape[1]:
+            lu["stopped"] = True
+            return
+        if j == 0:
+            lu["p1"] = max(gmax, 0.0)
+        if not (lu["p1"] > 0.0 and gmax > lu["p1"] * WP):
+            lu["stopped"] = True
+            return
+        mine = owner == (dist.get_rank() if self.dist else 0)
+        pv = urow[-1]
+        mult = w[:, j] / pv
+        mult[lu["chosen"]] = 0.0
+        if mine:
+            mult[lu["idx"]] = 1.0
+            lu["chosen"][lu["idx"]] = True
+        lu["L"][:, j] = mult
+        w[:, j + 1:] -= np.outer(mult, urow[j + 1:w.shape[1]])
+        lu["r"] = j + 1
+
+    def lu_allreduce(self, what, count):
+        lu = self.lu
+        if what == "lu_max":
+            t = torch.tensor([lu["val"]], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            lu["gmax"] = float(t.item())
+        elif what == "lu_owner":
+            mine = lu["val"] >= 0.0 and lu["val"] == lu["gmax"]
+            t = torch.tensor([dist.get_rank() if mine else 2 ** 31 - 1], dtype=torch.int32)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            lu["owner"] = int(t.item())
+        else:  # lu_row: the owner's pivot row (+ the signed pivot), zeros elsewhere
+            w = lu["W"]
+            assert count >= w.shape[1] + 1, (count, w.shape)
+            row = np.zeros(count)
+            if lu["owner"] == dist.get_rank() and lu["idx"] >= 0 and lu["j"] < w.shape[1]:
+                row[:w.shape[1]] = w[lu["idx"]]
+                row[count - 1] = w[lu["idx"], lu["j"]]
+            t = torch.from_numpy(row)
+            dist.all_reduce(t)
+            u = t.numpy()
+            self.lu_step(lu["gmax"], lu["owner"], np.concatenate([u[:w.shape[1]], u[count - 1:]]))
+
     # -- collectives
     def allreduce(self, what, count):
+        if what.startswith("lu_"):
+            self.collectives.append((what, count))
+            return self.lu_allreduce(what, count)
         self.collectives.append((what, count))
         if what == "m":
             t = torch.tensor([self.a.shape[0]], dtype=torch.int64)
@@ -156,6 +219,24 @@ class Replay:
             return self.run_tsqr(tok)
         if k == "allreduce":
             self.allreduce(parts[1], int(parts[2]))
+        elif k == "lu_core":
+            self.mode = "lu"
+            self.dist = parts[1] == "sharded"
+            x = self.cur if self.cur is not None else self.a
+            self.lu = dict(W=np.array(x, dtype=np.float64), chosen=np.zeros(x.shape[0], dtype=bool),
+                           L=np.zeros(x.shape), r=0, stopped=False, p1=0.0)
+        elif k == "lu_col":
+            self.lu_local(int(parts[1]))
+            if not self.dist:  # single rank: the decision and the update right away
+                lu = self.lu
+                w = lu["W"]
+                if lu["idx"] >= 0 and lu["j"] < w.shape[1]:
+                    urow = np.concatenate([w[lu["idx"]], [w[lu["idx"], lu["j"]]]])
+                else:
+                    urow = np.zeros(w.shape[1] + 1)
+                self.lu_step(lu["val"], 0, urow)
+        elif k == "lu_finish":
+            self.out = dict(U=self.lu["L"][:, :self.lu["r"]])
         elif k == "core":
             self.mode = "gram"
             self.dist = parts[1] == "sharded"
@@ -376,6 +457,29 @@ def test_two_rank_lowrank_tsqr_trace_replay():
     d = synth.config_inputs("c3", m=m, n=n)
     ref = oracle.lowrank_svd_tsqr(d["A"], d["Omega"], cfg["iters"], cfg["k"],
                                   lambda w: synth.mixing_params(w, MIX_SEED), WP)
+    assert s0.size == ref[1].size == cfg["k"]
+    assert_lowrank_parity((np.vstack([u0, u1]), s0, v0), ref, d["A"], d["x0"])
+
+
+def test_two_rank_lowrank_lu_trace_replay():
+    """lowrank_svd_lu (Alg. 8 with LU-based tracking) on 2 ranks from the trace:
+    partial pivoting across the row shards (MAX of the candidates' magnitudes, MIN of the owning
+    rank, the pivot row summed from its owner), the replicated n x l eliminations local, one round
+    trip; the single-process LU oracle reproduced."""
+    import oracle
+    import synth
+
+    m, n = 8_000, 1_001
+    res = _run_world("lowrank_lu", "c3", m, n)
+    (_, t0, c0, s0, v0, u0, o0), (_, t1, c1, s1, v1, u1, o1) = res
+    assert t0 == t1 and _syncs(t0) == [] and t0[-1] == "finish"
+    cfg = synth.CONFIGS["c3"]
+    whats = [w for w, _ in c0]
+    assert whats.count("lu_max") == whats.count("lu_owner") == whats.count("lu_row") == cfg["iters"] * cfg["l"]
+    assert np.array_equal(s0, s1) and np.array_equal(v0, v1)
+    assert o0 <= 1e-13
+    d = synth.config_inputs("c3", m=m, n=n)
+    ref = oracle.lowrank_svd_lu(d["A"], d["Omega"], cfg["iters"], cfg["k"], WP)
     assert s0.size == ref[1].size == cfg["k"]
     assert_lowrank_parity((np.vstack([u0, u1]), s0, v0), ref, d["A"], d["x0"])
 

@@ -435,3 +435,56 @@ def test_paper_alg7(key, l):
     assert err == pytest.approx(g["spectral_error"], rel=5e-3)
     assert abs(err - sig[s.size]) <= 1e-3 * sig[s.size]
     assert oracle.ortho_error(u) <= 1e-14 and oracle.ortho_error(v) <= 1e-14
+
+
+# ----------------------------------------------- LU-based subspace tracking --
+def test_lu_tracking_factor_is_lapack_gepp():
+    """P:405-409 (reading R21): the L of Gaussian elimination with partial pivoting.  Special
+    case that reduces to a library routine: LAPACK dgetrf (scipy.linalg.lu, Y = P L U) picks the
+    same pivots, so the oracle's L (Y's row order) equals P L; partial pivoting bounds |L| <= 1;
+    the column space of L is Y's (projection residual at rounding level)."""
+    import scipy.linalg as sl
+
+    rng = np.random.default_rng(21)
+    for m, l in [(50, 6), (400, 25), (1000, 60), (7, 7)]:
+        y = rng.standard_normal((m, l)) * np.logspace(0, -4, l)[None, :]
+        lm, r = oracle.lu_tracking_factor(y, 1e-11)
+        p, ls, u = sl.lu(y)
+        assert r == l
+        assert np.max(np.abs(lm - p @ ls)) <= 1e-13
+        assert np.max(np.abs(lm)) <= 1.0
+        q = np.linalg.qr(lm)[0]
+        assert np.linalg.norm(y - q @ (q.T @ y), 2) <= 1e-13 * np.linalg.norm(y, 2)
+
+
+def test_lu_tracking_factor_rank_deficient():
+    """A numerically zero pivot stops the elimination (R21): rank-3 Y with 6 columns keeps 3
+    columns spanning Y's column space; Y = 0 keeps none."""
+    rng = np.random.default_rng(22)
+    y = rng.standard_normal((300, 3)) @ rng.standard_normal((3, 6))
+    lm, r = oracle.lu_tracking_factor(y, 1e-11)
+    assert r == 3 and lm.shape == (300, 3)
+    q = np.linalg.qr(lm)[0]
+    assert np.linalg.norm(y - q @ (q.T @ y), 2) <= 1e-12 * np.linalg.norm(y, 2)
+    assert oracle.lu_tracking_factor(np.zeros((10, 4)))[1] == 0
+
+
+def test_lowrank_lu_equals_alg8():
+    """'the column space of L is the same as the column space of Q', so Alg. 8 with
+    LU tracking returns Alg. 8's result: on c3's spectrum (reduced) sigma agrees to 1e-13 sigma_1
+    and U, V columns within the R12 bound; on the paper's Table 8 matrix (m = 1e4, n = 2000,
+    l = 20, i = 2) the residual is the printed 4.83e-07."""
+    d = synth.config_inputs("c3", m=20_000, n=2_000)
+    ref = oracle.lowrank_svd(d["A"], d["Omega"], d["iters"], d["k"])
+    lu = oracle.lowrank_svd_lu(d["A"], d["Omega"], d["iters"], d["k"])
+    assert lu[1].size == ref[1].size
+    assert np.max(np.abs(lu[1] - ref[1])) <= 1e-13 * ref[1][0]
+    bound = 1e3 * np.finfo(float).eps * (ref[1][0] / ref[1]) ** 2
+    for g, r in ((lu[0], ref[0]), (lu[2], ref[2])):
+        dist = np.minimum(np.linalg.norm(g - r, axis=0), np.linalg.norm(g + r, axis=0))
+        assert np.all(dist <= bound)
+    g = PAPER["alg8_l20_i2_m1e4_n2000"]
+    a, _ = synth.paper_lowrank_test_matrix(g["m"], g["n"], g["l"])
+    u, s, v = oracle.lowrank_svd_lu(a, synth.omega(g["n"], g["l"], 1), g["i"], g["l"])
+    err = oracle.spectral_error(a, u, s, v, synth.power_start(g["n"], 7))
+    assert err == pytest.approx(g["spectral_error"], rel=5e-3)

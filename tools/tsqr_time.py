@@ -71,5 +71,12 @@ for cfg in which:
         set_pass_timing(False)
         pl = passes_line()
         tg = timeit(lambda: tk.lowrank_svd(A, Om, c["iters"], k=c["k"]))
+        tl = timeit(lambda: tk.lowrank_svd(A, Om, c["iters"], k=c["k"], tracking="lu"))
+        set_pass_timing(True)
+        tk.lowrank_svd(A, Om, c["iters"], k=c["k"], tracking="lu")
+        torch.cuda.synchronize()
+        set_pass_timing(False)
+        pll = passes_line()
         print(f"{cfg} alg7 min/med {t[0]:.2f}/{t[1]:.2f} ms; alg8 {tg[0]:.2f}/{tg[1]:.2f} ms; passes {pl}",
               flush=True)
+        print(f"{cfg} alg8 with LU tracking min/med {tl[0]:.2f}/{tl[1]:.2f} ms; passes {pll}", flush=True)
