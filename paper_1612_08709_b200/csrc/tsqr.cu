@@ -188,10 +188,12 @@ __global__ void __launch_bounds__(MAXT, 1) k_leaf_qr(double* X, int64_t ldx, int
       }
       __syncwarp();
       constexpr int RL = B / 32;  // rows per lane: i = lane + 32 r
+#pragma unroll  // kq compile-time: the accumulator slots below stay in registers
       for (int kq = 0; kq < 4; ++kq) {
         const int col = p + kq;
         if (col >= kmax) {  // absent reflector: H = I (tau 0, zero column of T)
           if (lane == 0)
+#pragma unroll
             for (int i2 = 0; i2 < 4; ++i2) T[4 * i2 + kq] = 0.0;
           continue;
         }
