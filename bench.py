@@ -49,6 +49,10 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-clocks", action="store_true", help="diagnosis: no clock sampling")
     p.add_argument("--cpu-sample-rows", type=int, default=0)
+    p.add_argument("--method", default="gram", choices=["gram", "tsqr", "lu"],
+                   help="gram: Alg. 4 / Alg. 8 (the north star); tsqr: Alg. 2 / Alg. 7 (randomized "
+                        "TSQR, n <= 128 for tall-skinny configs); lu: Alg. 8 with LU-based tracking "
+                        "(low-rank configs)")
     return p.parse_args()
 
 
@@ -157,8 +161,29 @@ def _gbytes(line, key):
     return float(v)
 
 
-def a_passes(cfg):
-    return 2 if cfg["kind"] == "tssvd" else 2 * cfg["iters"] + 2
+def a_passes(cfg, method="gram"):
+    # passes over A itself: Alg. 4 two Gram passes; Alg. 2 one (B* = A Omega*; its TSQRs work on
+    # B* / Q); Alg. 5 + 6 (any factorization): 2 i + 2
+    if cfg["kind"] == "tssvd":
+        return 1 if method == "tsqr" else 2
+    return 2 * cfg["iters"] + 2
+
+
+MIX_SEED = 17  # the draws of Omega = D F S D~ F S~ for the TSQR-based algorithms
+
+
+def oracle_step(oracle, cfg, d, a, method, wp):
+    if cfg["kind"] == "tssvd":
+        if method == "tsqr":
+            oracle.tsqr_svd(a, *synth.mixing_params(a.shape[1], MIX_SEED), wp, 2)
+        else:
+            oracle.tssvd(a, wp, 2)
+    elif method == "tsqr":
+        oracle.lowrank_svd_tsqr(a, d["Omega"], d["iters"], d["k"], lambda w: synth.mixing_params(w, MIX_SEED), wp)
+    elif method == "lu":
+        oracle.lowrank_svd_lu(a, d["Omega"], d["iters"], d["k"], wp)
+    else:
+        oracle.lowrank_svd(a, d["Omega"], d["iters"], d["k"], wp)
 
 
 # ------------------------------------------------------------ reference --
@@ -186,10 +211,7 @@ def run_reference(args, rank, world):
     a = d["A"]
 
     def step():
-        if cfg["kind"] == "tssvd":
-            oracle.tssvd(a, cfg.get("wp", args.wp), 2)
-        else:
-            oracle.lowrank_svd(a, d["Omega"], d["iters"], d["k"], args.wp)
+        oracle_step(oracle, cfg, d, a, args.method, cfg.get("wp", args.wp))
 
     for _ in range(args.warmup):
         step()
@@ -198,9 +220,9 @@ def run_reference(args, rank, world):
         step()
     dt = (time.perf_counter() - t0) / args.steps
     cpu_s = (time.process_time() - c0) / args.steps
-    gbs = a_passes(cfg) * a.nbytes / dt / 1e9
+    gbs = a_passes(cfg, args.method) * a.nbytes / dt / 1e9
     sample = f"first {a.shape[0]} rows x {a.shape[1]} cols of {args.config} ({a.nbytes / 1e9:.2f} GB)"
-    line = {"impl": "reference", "metric": metric_name(cfg), "value": round(gbs, 3), "unit": "GB/s",
+    line = {"impl": "reference", "metric": metric_name(cfg, args.method), "value": round(gbs, 3), "unit": "GB/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -213,17 +235,23 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def metric_name(cfg):
-    return "A-stream GB/s (Alg. 4 tall-skinny SVD)" if cfg["kind"] == "tssvd" else \
-        "A-stream GB/s (Alg. 8 low-rank SVD)"
+def metric_name(cfg, method="gram"):
+    if cfg["kind"] == "tssvd":
+        return "A-stream GB/s (Alg. 2 TSQR-based tall-skinny SVD)" if method == "tsqr" else \
+            "A-stream GB/s (Alg. 4 tall-skinny SVD)"
+    return {"tsqr": "A-stream GB/s (Alg. 7 low-rank SVD)",
+            "lu": "A-stream GB/s (Alg. 8 low-rank SVD, LU-based tracking)"}.get(
+        method, "A-stream GB/s (Alg. 8 low-rank SVD)")
 
 
 def config_obj(args, cfg, world):
     paper = {"t3": "PAPER Table 3", "t4": "PAPER Table 4", "t5": "PAPER Table 5",
              "s21": "PAPER Table 21 (Devil's staircase)"}.get(args.config)
+    alg_t = "Alg. 2 (random mixing, two TSQRs)" if args.method == "tsqr" else "Alg. 4 (two Gram passes)"
+    alg_l = {"tsqr": "Alg. 7", "lu": "Alg. 8 with LU-based tracking (P:405-409)"}.get(args.method, "Alg. 8")
     c = {"workload": f"{args.config}: {cfg['m']}x{cfg['n']} FP64 "
-                     + ("tall-skinny SVD, Alg. 4 (two Gram passes)" if cfg["kind"] == "tssvd"
-                        else f"low-rank SVD Alg. 8, k={cfg['k']} l={cfg['l']} i={cfg['iters']}")
+                     + (f"tall-skinny SVD, {alg_t}" if cfg["kind"] == "tssvd"
+                        else f"low-rank SVD {alg_l}, k={cfg['k']} l={cfg['l']} i={cfg['iters']}")
                      + (f", {paper} matrix (Eq. originalmat, DCT factors)" if paper else ""),
          "m": cfg["m"], "n": cfg["n"], "rows_per_gpu": -(-cfg["m"] // world),
          "working_precision": cfg.get("wp", args.wp), "parallelism": f"row-shard x{world}",
@@ -255,10 +283,26 @@ def run_ours(args, rank, world, local_rank):
     U = torch.empty_like(A) if not lowrank else None
 
     wp = cfg.get("wp", args.wp)  # the paper workloads fix their own (reading Q1)
+    method = args.method
+    if method == "tsqr" and not lowrank and n > 128:
+        raise SystemExit(f"--method tsqr: tall-skinny configs need n <= 128 ({args.config} has n = {n})")
+    if method == "lu" and not lowrank:
+        raise SystemExit("--method lu applies to the low-rank configs")
+    if method == "tsqr":
+        if lowrank:
+            ph, pm = tk.mixing_tables(lambda w: synth.mixing_params(w, MIX_SEED), cfg["l"], dev)
+        else:
+            ph_np, pm_np = synth.mixing_params(n, MIX_SEED)
+            ph, pm = torch.from_numpy(ph_np).to(dev), torch.from_numpy(pm_np).to(dev)
 
     def step():
         if lowrank:
-            return tk.lowrank_svd(A, Om, cfg["iters"], cfg["k"], wp=wp, comm=comm)
+            if method == "tsqr":
+                return tk.lowrank_svd_tsqr(A, Om, cfg["iters"], ph, pm, k=cfg["k"], wp=wp, comm=comm)
+            return tk.lowrank_svd(A, Om, cfg["iters"], cfg["k"], wp=wp, comm=comm,
+                                  tracking="lu" if method == "lu" else "q")
+        if method == "tsqr":
+            return tk.tsqr_svd(A, ph, pm, wp=wp, passes=2, comm=comm)
         return tk.tssvd(A, wp=wp, passes=2, comm=comm, U=U)
 
     def barrier():
@@ -300,12 +344,15 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t = tt.item()
-    total_a_bytes = 8.0 * cfg["m"] * cfg["n"] * a_passes(cfg)
+    total_a_bytes = 8.0 * cfg["m"] * cfg["n"] * a_passes(cfg, method)
     value = total_a_bytes / (t * 1e-3) / 1e9
 
     # e2e through the same C-ABI call with HOST buffers (H2D of A, D2H of U/sigma/V inside)
     e2e = None
-    if not args.no_e2e:
+    if method == "tsqr":
+        e2e = {"value": None, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+               "unavailable": "the TSQR entry points take device pointers only (host_io 0)"}
+    elif not args.no_e2e:
         ts = []
         ew = max(2, min(args.warmup, 3))  # >= 2: the pinned output blocks of two calls are live
         for i in range(ew + args.steps):
@@ -314,7 +361,7 @@ def run_ours(args, rank, world, local_rank):
             s0.record(stream)
             if lowrank:
                 u_h, s_h, v_h = tk.lowrank_svd(a_host, om_host, cfg["iters"], cfg["k"], wp=wp,
-                                               comm=comm)
+                                               comm=comm, tracking="lu" if method == "lu" else "q")
             else:
                 u_h, s_h, v_h = tk.tssvd(a_host, wp=wp, passes=2, comm=comm)
             s1.record(stream)
@@ -345,7 +392,7 @@ def run_ours(args, rank, world, local_rank):
 
     achieved = rate(dom)
     traffic, traffic_src = ncu_traffic(args.config, dom)
-    roof = {"kernel": dom, "bound": "tensor", "achieved": round(achieved, 3),
+    roof = {"kernel": dom, "bound": "alu" if dom == "tsqr" else "tensor", "achieved": round(achieved, 3),
             "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
             "traffic": traffic, "traffic_source": traffic_src,
             "algorithmic_bytes_per_launch": round(statistics.mean(
@@ -361,7 +408,7 @@ def run_ours(args, rank, world, local_rank):
     # Alg. 3 vs Alg. 4 orthonormality (BASELINE configs[1]): max|U^T U - I| after one and after
     # two Gram passes, measured with a cuBLAS Gram outside the timed region
     ortho = None
-    if not lowrank and world == 1:
+    if not lowrank and world == 1 and method == "gram":
         ortho = {}
         for npass in (1, 2):
             u1, s1_, _ = tk.tssvd(A, wp=wp, passes=npass, U=U)
@@ -373,7 +420,7 @@ def run_ours(args, rank, world, local_rank):
         cpu = cpu_baseline(args, cfg)
 
     if rank == 0:
-        line = {"metric": metric_name(cfg), "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
+        line = {"metric": metric_name(cfg, method), "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t, 4),
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": config_obj(args, cfg, world),
@@ -402,16 +449,13 @@ def cpu_baseline(args, cfg):
     a = d["A"]
     reps, t0, c0 = 0, time.perf_counter(), time.process_time()
     while True:
-        if cfg["kind"] == "tssvd":
-            oracle.tssvd(a, cfg.get("wp", args.wp), 2)
-        else:
-            oracle.lowrank_svd(a, d["Omega"], d["iters"], d["k"], args.wp)
+        oracle_step(oracle, cfg, d, a, args.method, cfg.get("wp", args.wp))
         reps += 1
         if time.perf_counter() - t0 > 10.0 or reps >= 20:
             break
     dt = (time.perf_counter() - t0) / reps
     cpu_s = (time.process_time() - c0) / reps
-    return {"value": round(a_passes(cfg) * a.nbytes / dt / 1e9, 3), "unit": "GB/s",
+    return {"value": round(a_passes(cfg, args.method) * a.nbytes / dt / 1e9, 3), "unit": "GB/s",
             "cores": os.cpu_count(), "kind": "oracle", "cpu_model": cpu_model(),
             "wall_s_per_step": round(dt, 3), "cpu_s_per_step": round(cpu_s, 3),
             "sample": f"{reps} oracle runs on the first {a.shape[0]} rows x {a.shape[1]} cols of "
