@@ -41,6 +41,39 @@ __global__ void dmma_kernel(double* out, int iters) {
   if (s == 12345.678) out[0] = s;
 }
 
+
+// Mixed: warps with (warp & 1) == 0 issue DMMA, the others DFMA -- do the two share one pipe?
+template <int TILES, int CHAINS>
+__global__ void mixed_kernel(double* out, int iters_mma, int iters_fma, double a0, double b0) {
+  int warp = threadIdx.x >> 5;
+  double s = 0;
+  if ((warp & 1) == 0) {
+    double c[TILES][2];
+    double a = threadIdx.x * 1e-3, b = 1.0 - threadIdx.x * 1e-4;
+#pragma unroll
+    for (int t = 0; t < TILES; ++t) { c[t][0] = 0; c[t][1] = t; }
+    for (int i = 0; i < iters_mma; ++i) {
+#pragma unroll
+      for (int t = 0; t < TILES; ++t)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c[t][0]), "+d"(c[t][1]) : "d"(a), "d"(b));
+    }
+#pragma unroll
+    for (int t = 0; t < TILES; ++t) s += c[t][0] + c[t][1];
+  } else {
+    double acc[CHAINS];
+#pragma unroll
+    for (int c = 0; c < CHAINS; ++c) acc[c] = threadIdx.x * 1e-3 + c;
+    for (int i = 0; i < iters_fma; ++i) {
+#pragma unroll
+      for (int c = 0; c < CHAINS; ++c) acc[c] = fma(acc[c], a0, b0);
+    }
+#pragma unroll
+    for (int c = 0; c < CHAINS; ++c) s += acc[c];
+  }
+  if (s == 12345.678) out[0] = s;
+}
+
 __global__ void read_kernel(const double2* __restrict__ p, size_t n, double* out) {
   double s = 0;
   size_t stride = (size_t)gridDim.x * blockDim.x;
@@ -92,6 +125,19 @@ int main() {
     CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1);
     double flops = 10.0 * blocks * threads * (double)iters * 8 * 2;
     printf("DFMA sustained (%.1f s): %.2f TFLOP/s\n", ms * 1e-3, flops / (ms * 1e-3) / 1e12);
+  }
+
+  // Mixed DMMA + DFMA warps in the same CTAs: if the sum exceeds the DMMA peak, the pipes are separate.
+  for (int fi : {0, 5000, 10000, 20000, 40000}) {
+    int blocks = sms * 2, threads = 512, im = 20000;
+    mixed_kernel<8, 8><<<blocks, threads>>>(out, 100, fi ? 100 : 0, 1.0000001, 1e-9);
+    CK(cudaEventRecord(e0));
+    for (int r = 0; r < 5; ++r) mixed_kernel<8, 8><<<blocks, threads>>>(out, im, fi, 1.0000001, 1e-9);
+    CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1)); cudaEventElapsedTime(&ms, e0, e1);
+    double fm = 5.0 * blocks * (threads / 64) * (double)im * 8 * 512;
+    double ff = 5.0 * blocks * (threads / 2) * (double)fi * 8 * 2;
+    printf("MIXED dmma iters=%d dfma iters=%d: %.3f ms, DMMA %.2f + DFMA %.2f = %.2f TFLOP/s\n", im, fi, ms,
+           fm / (ms * 1e-3) / 1e12, ff / (ms * 1e-3) / 1e12, (fm + ff) / (ms * 1e-3) / 1e12);
   }
   // HBM read
   size_t bytes = (size_t)8 << 30;
