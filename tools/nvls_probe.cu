@@ -40,23 +40,39 @@ int main() {
   const int n = 1 << 16;
   CUmulticastObjectProp mp = {};
   mp.numDevices = 1;
-  mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
   size_t gran = 0;
-  CU(cuMulticastGetGranularity(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED));
-  size_t size = ((n * 8 + gran - 1) / gran) * gran;
-  mp.size = size;
-  printf("granularity=%zu size=%zu\n", gran, size);
   CUmemGenericAllocationHandle mch;
-  CU(cuMulticastCreate(&mch, &mp));
+  const char* names[3] = {"none", "posix_fd", "fabric"};
+  CUmemAllocationHandleType types[3] = {CU_MEM_HANDLE_TYPE_NONE, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR,
+                                        CU_MEM_HANDLE_TYPE_FABRIC};
+  int ok = -1;
+  size_t size = 0;
+  for (int ti = 2; ti >= 0; --ti) {
+    mp.handleTypes = types[ti];
+    mp.size = 0;
+    CUresult rg = cuMulticastGetGranularity(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED);
+    size = ((n * 8 + gran - 1) / gran) * gran;
+    mp.size = size;
+    CUresult rc = cuMulticastCreate(&mch, &mp);
+    printf("cuMulticastCreate handleTypes=%s gran_rc=%d gran=%zu -> %d\n", names[ti], (int)rg, gran, (int)rc);
+    if (rc == CUDA_SUCCESS) { ok = ti; break; }
+  }
+  if (ok < 0) return 1;
   int fd = -1;
-  CUresult er = cuMemExportToShareableHandle(&fd, mch, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0);
-  printf("export mc handle as posix fd: rc=%d fd=%d\n", (int)er, fd);
+  if (ok == 1) {
+    CUresult er = cuMemExportToShareableHandle(&fd, mch, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0);
+    printf("export mc handle as posix fd: rc=%d fd=%d\n", (int)er, fd);
+  } else if (ok == 2) {
+    CUmemFabricHandle fh;
+    CUresult er = cuMemExportToShareableHandle(&fh, mch, CU_MEM_HANDLE_TYPE_FABRIC, 0);
+    printf("export mc handle as fabric handle: rc=%d\n", (int)er);
+  }
   CU(cuMulticastAddDevice(mch, dev));
   CUmemAllocationProp ap = {};
   ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
   ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   ap.location.id = dev;
-  ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  ap.requestedHandleTypes = types[ok];
   CUmemGenericAllocationHandle ph;
   CU(cuMemCreate(&ph, size, &ap, 0));
   CU(cuMulticastBindMem(mch, 0, ph, 0, size, 0));
