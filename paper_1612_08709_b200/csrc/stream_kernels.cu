@@ -152,13 +152,16 @@ __global__ void __launch_bounds__(512, MINB) syrk_kernel(const __grid_constant__
   ring_init(ring, nst, ncw);
 
   if (warp == 0) {  // ---- producer
-    if (lane == 0)
+    if (lane == 0) {
+      int b = 0;
+      uint32_t ph = 0;
       for (int s = 0; s < nsteps; ++s) {
-        const int b = s % nst, u = s / nst;
-        if (u > 0) mbar_wait(ring.empty(b), (u - 1) & 1);
+        if (s >= nst) mbar_wait(ring.empty(b), ph ^ 1u);
         mbar_arrive_expect_tx(ring.full(b), (uint32_t)(stage_d * 8));
         tma_load_2d(buf + b * stage_d, &tx, 0, (int)(r0 + (int64_t)s * SYRK_KR), ring.full(b));
+        if (++b == nst) b = 0, ph ^= 1u;
       }
+    }
     return;
   }
   // this warp's run of tiles [q0, q1) of the row-major lower triangle
@@ -188,9 +191,10 @@ __global__ void __launch_bounds__(512, MINB) syrk_kernel(const __grid_constant__
 #pragma unroll
   for (int k = 0; k < TPW; ++k) acc[k][0] = acc[k][1] = 0.0;
 
+  int b = 0;
+  uint32_t ph = 0;
   for (int s = 0; s < nsteps; ++s) {
-    const int b = s % nst;
-    mbar_wait(ring.full(b), (s / nst) & 1);
+    mbar_wait(ring.full(b), ph);
     const double* base = buf + b * stage_d + t * W + g;
     if (nt > 0) {
 #pragma unroll
@@ -209,6 +213,7 @@ __global__ void __launch_bounds__(512, MINB) syrk_kernel(const __grid_constant__
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(ring.empty(b));
+    if (++b == nst) b = 0, ph ^= 1u;
   }
 
   double* P = part + (size_t)rb * wp * wp;
@@ -451,12 +456,16 @@ __host__ __device__ constexpr int nn_cw(int mi, int niw, int wc) { return mi * n
 // its last), which gemm_nn_fixup sums in CTA (= K) order and stores.
 __host__ __device__ inline int64_t sk_u0(int b, int64_t units, int grid) { return units * b / grid; }
 
-template <int MI, int NIW, int WC, int XR, bool SK, int NN_CW = nn_cw(MI, NIW, WC)>
+// KCT > 0: the K chunk as a compile-time constant (stream-K launches with the planner's usual
+// chunks): every k-step of a stage is unrolled with immediate shared-memory offsets (the
+// zero-filled k-steps of the last chunk are computed: 0 x 0 adds nothing).
+template <int MI, int NIW, int WC, int XR, bool SK, int KCT = 0, int NN_CW = nn_cw(MI, NIW, WC)>
 __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
     const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tm, int64_t m, int k,
-    int KC, int kc_count, int LDM, int c, double* Y, int64_t ldy, double* __restrict__ norm_part,
+    int KC_rt, int kc_count, int LDM, int c, double* Y, int64_t ldy, double* __restrict__ norm_part,
     int nst, double* __restrict__ sk_rec) {
   extern __shared__ __align__(128) unsigned char smem[];
+  const int KC = KCT > 0 ? KCT : KC_rt;
   constexpr int RW = NN_CW / WC;
   constexpr int R = 8 * MI * RW;
   static_assert(XR == 0 || WC == 1, "remainder columns need a single column group");
@@ -473,28 +482,32 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
   const int64_t mytiles = blockIdx.x < ntiles ? ceil_div(ntiles - blockIdx.x, (int64_t)gridDim.x) : 0;
   const int64_t nsteps = sk ? sk_u0(blockIdx.x + 1, units, gridDim.x) - u0 : mytiles * kc_count;
   const int64_t first_tile = sk ? u0 / kc_count : -1;
-  // step s -> (row tile, K chunk)
-  auto unit = [&](int64_t s, int64_t& tile, int& chunk) {
-    if constexpr (SK) {
-      tile = (u0 + s) / kc_count;
-      chunk = (int)((u0 + s) % kc_count);
-    } else {
-      tile = blockIdx.x + (s / kc_count) * gridDim.x;
-      chunk = (int)(s % kc_count);
+  // Step s -> (row tile, K chunk) and (ring slot, phase), advanced incrementally: one
+  // division at the start instead of four 64-bit divisions per stage (ncu r2: the integer
+  // work of the stage boundaries was 10% of the alpha pass's issue samples).
+  struct Cursor {
+    int64_t tile;
+    int chunk, b;
+    uint32_t ph;
+  };
+  const Cursor cur0{sk ? first_tile : (int64_t)blockIdx.x, sk ? (int)(u0 % kc_count) : 0, 0, 0u};
+  auto advance = [&](Cursor& q) {
+    if (++q.chunk == kc_count) {
+      q.chunk = 0;
+      q.tile += sk ? 1 : (int64_t)gridDim.x;
     }
+    if (++q.b == nst) q.b = 0, q.ph ^= 1u;
   };
   ring_init(ring, nst, NN_CW);
 
   if (warp == NN_CW) {  // ---- producer (last warp)
-    if (lane == 0)
-      for (int64_t s = 0; s < nsteps; ++s) {
-        const int b = (int)(s % nst);
-        const int64_t u = s / nst;
-        if (u > 0) mbar_wait(ring.empty(b), (uint32_t)((u - 1) & 1));
-        int64_t tile;
-        int chunk;
-        unit(s, tile, chunk);
-        const int k0 = chunk * KC;
+    if (lane == 0) {
+      Cursor q = cur0;
+      for (int64_t s = 0; s < nsteps; ++s, advance(q)) {
+        const int b = q.b;
+        if (s >= nst) mbar_wait(ring.empty(b), q.ph ^ 1u);
+        const int64_t tile = q.tile;
+        const int k0 = q.chunk * KC;
         double* xs = buf + b * stage_d;
         mbar_arrive_expect_tx(ring.full(b), (uint32_t)(stage_d * 8));
         // the X box in TMA boxes of at most 256 rows (R = 384 with 12 consumer warps)
@@ -504,6 +517,7 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
           tma_load_2d(xs + h * RB * KC, &tx, k0, (int)(tile * R + h * RB), ring.full(b));
         tma_load_2d(xs + xs_d, &tm, 0, k0, ring.full(b));
       }
+    }
     return;
   }
   const int rg = warp % RW, cg = warp / RW;
@@ -532,21 +546,19 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
     for (int col = lane; col < NB * 8; col += 32) red[col] = 0.0;
 
   bool partial = false;  // stream-K: this CTA's part of the current tile misses chunks
-  for (int64_t s = 0; s < nsteps; ++s) {
-    const int b = (int)(s % nst);
-    mbar_wait(ring.full(b), (uint32_t)((s / nst) & 1));
+  Cursor q = cur0;
+  for (int64_t s = 0; s < nsteps; ++s, advance(q)) {
+    const int b = q.b;
+    mbar_wait(ring.full(b), q.ph);
     const double* xs = buf + b * stage_d + (rg * MI * 8 + g) * KC + t;
     const double* ms = buf + b * stage_d + xs_d + t * LDM + col0 + g;
     TCHECK(((rg * MI + MI - 1) * 8 + g) * KC + t + KC - 4 < xs_d && col0 + (NIW - 1) * 8 + g < LDM);
-    int64_t tile = 0;
-    int kc_here;
-    if constexpr (SK) {
-      unit(s, tile, kc_here);
+    int64_t tile = q.tile;
+    const int kc_here = q.chunk;
+    if constexpr (SK)
       if (s == 0 || kc_here == 0) partial = kc_here != 0;
-    } else {
-      kc_here = (int)(s % kc_count);
-    }
-    const int nks = min(KC / 4, (k - kc_here * KC + 3) / 4);  // k-steps holding real columns
+    // k-steps holding real columns (KCT: all of them, the zero-filled ones included)
+    const int nks = KCT > 0 ? KCT / 4 : min(KC / 4, (k - kc_here * KC + 3) / 4);
     // (software-pipelining the fragment loads, as gemm_tn does, measured slower
     // here: 7.9 -> 9.0 ms per c3 alpha pass.)  SK: the fragments of a k-step are loaded
     // before its first DMMA (c3 alpha 7.2 -> 6.9 ms); the same source order made the
@@ -571,7 +583,9 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
         }
       }
     }
-    else for (int kk = 0; kk < nks; ++kk) {
+    else
+#pragma unroll
+    for (int kk = 0; kk < nks; ++kk) {
       double a[MI], bfr[NIW], mv[XR > 0 ? XR : 1];
 #pragma unroll
       for (int j = 0; j < NIW; ++j) bfr[j] = ms[kk * 4 * LDM + j * 8];
@@ -619,7 +633,6 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
         }
       }
     } else if (kc_here == kc_count - 1) {  // tile complete: epilogue
-      if constexpr (!SK) tile = blockIdx.x + (s / kc_count) * gridDim.x;
       if (norm_part && NRM) {  // rows beyond m hold zeros (TMA zero fill): no masking needed
 #pragma unroll
         for (int j = 0; j < (NRM ? NIW : 1); ++j)
@@ -853,7 +866,12 @@ template <int MI, int NIW, int WC, int XR>
 static cudaError_t nn_go(const NnPlan& p, const CUtensorMap& tx, const CUtensorMap& tm, int64_t m,
                          int k, int c, double* Y, int64_t ldy, double* norm_part, double* sk_rec,
                          cudaStream_t s) {
-  auto kern = sk_rec ? gemm_nn_kernel<MI, NIW, WC, XR, true> : gemm_nn_kernel<MI, NIW, WC, XR, false>;
+  // stream-K with the planner's usual K chunks as compile-time constants (TSSVD_NN_KCT=0: runtime KC)
+  static const bool kct = !getenv("TSSVD_NN_KCT") || atoi(getenv("TSSVD_NN_KCT")) != 0;
+  auto kern = !sk_rec ? gemm_nn_kernel<MI, NIW, WC, XR, false>
+              : kct && p.KC == 20 ? gemm_nn_kernel<MI, NIW, WC, XR, true, 20>
+              : kct && p.KC == 28 ? gemm_nn_kernel<MI, NIW, WC, XR, true, 28>
+                                  : gemm_nn_kernel<MI, NIW, WC, XR, true>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
   if (e != cudaSuccess) return e;
   kern<<<p.grid, (nn_cw(MI, NIW, WC) + 1) * 32, p.smem, s>>>(tx, tm, m, k, p.KC, p.kcc, p.ldm, c, Y, ldy, norm_part,
@@ -947,11 +965,14 @@ cudaError_t launch_gemm_nn(const double* X, int64_t ldx, int64_t m, int k, const
 // are summed by a butterfly before the store).
 static constexpr int TN_CW = 12;  // 3 consumer warps per SMSP: 8 -> 12 took c3 beta 7.7 -> 6.7 ms/pass
 
-template <int MI, int NBL, int XR>
+// KRT > 0: rows per stage as a compile-time constant (the planner's usual 32): the k-steps of a
+// stage unroll with immediate shared-memory offsets.
+template <int MI, int NBL, int XR, int KRT = 0>
 __global__ void __launch_bounds__(32 * (TN_CW + 1)) gemm_tn_kernel(
     const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap ty, int64_t m, int n,
-    int64_t rps, double* __restrict__ part, int ldz, int64_t n_pad, int KR, int nst) {
+    int64_t rps, double* __restrict__ part, int ldz, int64_t n_pad, int KR_rt, int nst) {
   extern __shared__ __align__(128) unsigned char smem[];
+  const int KR = KRT > 0 ? KRT : KR_rt;
   constexpr int CB = 8 * MI * TN_CW;
   constexpr int LDXS = CB + 4;
   constexpr int LDYS = NBL * 8 + 4;
@@ -966,16 +987,19 @@ __global__ void __launch_bounds__(32 * (TN_CW + 1)) gemm_tn_kernel(
   ring_init(ring, nst, TN_CW);
 
   if (warp == TN_CW) {  // ---- producer
-    if (lane == 0)
-      for (int s = 0; s < nsteps; ++s) {
-        const int b = s % nst, u = s / nst;
-        if (u > 0) mbar_wait(ring.empty(b), (u - 1) & 1);
+    if (lane == 0) {
+      int b = 0;
+      uint32_t ph = 0;
+      for (int s = 0; s < nsteps; ++s) {  // ring slot and phase advanced incrementally
+        if (s >= nst) mbar_wait(ring.empty(b), ph ^ 1u);
         const int rs = (int)(r0 + (int64_t)s * KR);
         double* xs = buf + b * stage_d;
         mbar_arrive_expect_tx(ring.full(b), (uint32_t)(stage_d * 8));
         tma_load_2d(xs, &tx, c0, rs, ring.full(b));
         tma_load_2d(xs + xs_d, &ty, 0, rs, ring.full(b));
+        if (++b == nst) b = 0, ph ^= 1u;
       }
+    }
     return;
   }
 
@@ -990,9 +1014,10 @@ __global__ void __launch_bounds__(32 * (TN_CW + 1)) gemm_tn_kernel(
 #pragma unroll
     for (int x = 0; x < (XR > 0 ? XR : 1); ++x) ex[i][x] = 0.0;
 
+  int b = 0;
+  uint32_t ph = 0;
   for (int s = 0; s < nsteps; ++s) {
-    const int b = s % nst;
-    mbar_wait(ring.full(b), (s / nst) & 1);
+    mbar_wait(ring.full(b), ph);
     const double* xs = buf + b * stage_d + t * LDXS + warp * MI * 8 + g;
     const double* ys = buf + b * stage_d + xs_d + t * LDYS + g;
     // software-pipelined fragment loads, as in gemm_nn
@@ -1009,6 +1034,7 @@ __global__ void __launch_bounds__(32 * (TN_CW + 1)) gemm_tn_kernel(
         for (int x = 0; x < XR; ++x) fy[x] = ys[q * 4 * LDYS + NBL * 8 + x - g];
     };
     load(0, a, bf, yv);
+#pragma unroll
     for (int kk = 0; kk < nkk; ++kk) {
       double an[MI], bn[NBL], yn[XRA];
       load(min(kk + 1, nkk - 1), an, bn, yn);
@@ -1030,6 +1056,7 @@ __global__ void __launch_bounds__(32 * (TN_CW + 1)) gemm_tn_kernel(
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(ring.empty(b));
+    if (++b == nst) b = 0, ph ^= 1u;
   }
 
   double* P = part + (size_t)blockIdx.y * n_pad * ldz;
@@ -1098,7 +1125,8 @@ template <int MI, int NBL, int XR = 0>
 static cudaError_t tn_go(const TnPlan& p, const CUtensorMap& tx, const CUtensorMap& ty, int64_t m, int n,
                          double* part, cudaStream_t s) {
   const size_t smem = kBarBytes + (size_t)p.nst * p.kr * ((p.cb + 4) + (NBL * 8 + 4)) * 8;
-  auto kern = gemm_tn_kernel<MI, NBL, XR>;
+  static const bool krt = !getenv("TSSVD_TN_KRT") || atoi(getenv("TSSVD_TN_KRT")) != 0;  // experiments
+  auto kern = krt && p.kr == 32 ? gemm_tn_kernel<MI, NBL, XR, 32> : gemm_tn_kernel<MI, NBL, XR>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid(p.colblocks, p.splits);
