@@ -270,6 +270,18 @@ int tssvd_sym_eig(void* stream, int64_t n, const double* B, int64_t ldb, double*
                   size_t workspace_bytes);
 size_t tssvd_sym_eig_workspace(int64_t n);
 
+/* Eigendecomposition of a symmetric PSD matrix by Householder tridiagonalisation and the
+ * implicit QL iteration (one CTA; the solver tssvd() uses for Alg. 4 step 8, P:670-672,
+ * "Calculate the eigendecomposition Z = W D W^*", where Z = Y^* Y is near the identity and
+ * one-sided Jacobi converges only linearly).  Same layout and outputs as tssvd_sym_eig:
+ * lambda[j] descending (values <= eps * max diag(B) returned as 0 with a zero row), row j of Vt
+ * (ld ldv) = eigenvector j.  1 <= n <= 160.  *iterations (may be NULL) = QL iterations.
+ * Workspace: tssvd_sym_eig_workspace(n) bytes.  Errors: TSSVD_EINVAL (n, ld), TSSVD_ENOMEM
+ * (workspace), TSSVD_ENONFINITE (Inf/NaN in B), TSSVD_ENOCONV (an eigenvalue not deflated in
+ * 30 QL iterations). */
+int tssvd_sym_eig_ql(void* stream, int64_t n, const double* B, int64_t ldb, double* lambda,
+                     double* Vt, int64_t ldv, int* iterations, void* workspace, size_t workspace_bytes);
+
 /* Plan-only run (no GPU, no CUDA or NCCL call): the steps and collectives that
  * tssvd() (problem = 1; l, iters, k ignored), lowrank_svd() (2), tsqr_svd() (3),
  * lowrank_svd_tsqr() (4) or lowrank_svd_lu() (5) would

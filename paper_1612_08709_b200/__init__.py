@@ -6,8 +6,8 @@ The product is the C-ABI library lib/libtssvd_b200.so (include/tssvd.h); this
 package is its thin ctypes/torch binding.  There is no CPU fallback.
 """
 from .api import (Comm, gram, last_stats, lowrank_svd, lowrank_svd_tsqr, matmul, matmul_tn,  # noqa: F401
-                  mixing_tables, sym_eig, tsqr_svd, tssvd)
+                  mixing_tables, sym_eig, sym_eig_ql, tsqr_svd, tssvd)
 from .partition import shard_rows  # noqa: F401
 
-__all__ = ["Comm", "tssvd", "lowrank_svd", "tsqr_svd", "lowrank_svd_tsqr", "mixing_tables", "gram", "matmul", "matmul_tn", "sym_eig",
+__all__ = ["Comm", "tssvd", "lowrank_svd", "tsqr_svd", "lowrank_svd_tsqr", "mixing_tables", "gram", "matmul", "matmul_tn", "sym_eig", "sym_eig_ql",
            "last_stats", "shard_rows"]

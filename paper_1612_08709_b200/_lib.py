@@ -94,6 +94,8 @@ SIGNATURES = [
     ("tssvd_sym_eig", c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_int64,
                               c_int, P(c_int), c_void_p, c_size_t]),
     ("tssvd_sym_eig_workspace", c_size_t, [c_int64]),
+    ("tssvd_sym_eig_ql", c_int, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_void_p, c_int64,
+                                 P(c_int), c_void_p, c_size_t]),
     ("tssvd_trace", c_int, [c_int, c_int, c_int64, c_int64, c_int64, c_int, c_int64, P(TssvdOpts),
                             c_char_p, c_size_t]),
 ]

@@ -322,4 +322,18 @@ def sym_eig(B: torch.Tensor, max_sweeps: int = 60):
     return lam, Vt.T, sw.value
 
 
+def sym_eig_ql(B: torch.Tensor):
+    """Eigendecomposition of a symmetric PSD matrix (n <= 160) by tridiagonalisation + implicit QL,
+    the solver of Alg. 4 step 8: (lambda desc, V with eigvec columns, QL iterations)."""
+    n = B.shape[0]
+    lam = torch.empty(n, dtype=torch.float64, device=B.device)
+    Vt = torch.empty((n, n), dtype=torch.float64, device=B.device)
+    ws = _workspace(lib().tssvd_sym_eig_workspace(n), B.device)
+    it = ctypes.c_int()
+    Bc = B.contiguous()
+    check(lib().tssvd_sym_eig_ql(_stream(B.device), n, Bc.data_ptr(), n, lam.data_ptr(),
+                                 Vt.data_ptr(), n, ctypes.byref(it), ws.data_ptr(), ws.numel()))
+    return lam, Vt.T, it.value
+
+
 last_stats = _lib.last_stats

@@ -413,13 +413,24 @@ inline double jacobi_tol(int rows) { return std::max(8.0, 2.0 * std::sqrt((doubl
 // reading R13).  sync = true: one round trip returns k (it sizes the next GEMM);
 // sync = false: returns the bound n, convergence is checked at the end of the call.
 // *nf_flag receives the device address of the solve's non-finite flag.
+// Alg. 4 step 8 on Z = Y^* Y ~ I: one-sided Jacobi by default; TSSVD_ZEIG=ql selects the
+// tridiagonal QL solver (tridiag_eig.cu), which deflates regardless of Z's clustered spectrum
+// (Jacobi needs 11-14 sweeps at c2) but measured slower on one CTA (c2: 0.64 vs 0.50 ms).
+static bool z_by_ql(int n) {
+  static const bool ql = getenv("TSSVD_ZEIG") && strcmp(getenv("TSSVD_ZEIG"), "ql") == 0;
+  return ql && n <= kTridiagMax;
+}
+
 int eig(Ctx& c, Core& b, double* B, int n, double* vals, double trunc_rel, bool sync, const int** nf_flag,
         const char* what) {
   step("eig:%s", what);
   int* info = sync ? b.info : c.next_info();
   {
     Pass t(c.s, TSSVD_PASS_JACOBI, 0, 0);
-    KL(launch_jacobi_eig(B, n, n, jacobi_tol(n), trunc_rel, c.max_sweeps, B, n, vals, info, c.s));
+    if (what[0] == 'Z' && z_by_ql(n))
+      KL(launch_tridiag_eig(B, n, n, trunc_rel, B, n, vals, info, c.s));
+    else
+      KL(launch_jacobi_eig(B, n, n, jacobi_tol(n), trunc_rel, c.max_sweeps, B, n, vals, info, c.s));
   }
   *nf_flag = info + 6;
   if (!sync) return n;
@@ -696,7 +707,9 @@ int wide_eig(Ctx& c, WideCore& b, double* Bm, int n, double* vals, double trunc,
   int* info = sync ? b.info : c.next_info();
   {
     Pass t(c.s, TSSVD_PASS_JACOBI, 0, 0);
-    if (n <= 256)
+    if (what[0] == 'Z' && z_by_ql(n))
+      KL(launch_tridiag_eig(Bm, n, n, trunc, Bm, n, vals, info, c.s));
+    else if (n <= 256)
       KL(launch_jacobi_eig(Bm, n, n, jacobi_tol(n), trunc, c.max_sweeps, Bm, n, vals, info, c.s));
     else
       KL(launch_jacobi_eig_wide(Bm, n, n, jacobi_tol(n), trunc, c.max_sweeps, Bm, n, vals, info, b.jw, c.s));
@@ -1904,6 +1917,27 @@ int tssvd_sym_eig(void* stream, int64_t n, const double* B, int64_t ldb, double*
     CU(cudaStreamSynchronize(s));
     if (sweeps) *sweeps = h[0];
     if (!h[1]) fail(TSSVD_ENOCONV, "sym_eig did not converge");
+  });
+}
+
+int tssvd_sym_eig_ql(void* stream, int64_t n, const double* B, int64_t ldb, double* lambda, double* Vt,
+                     int64_t ldv, int* iterations, void* ws, size_t wsb) {
+  return guarded([&] {
+    if (n < 1 || n > kTridiagMax || ldb < n || ldv < n)
+      fail(TSSVD_EINVAL, "bad sym_eig_ql arguments (1 <= n <= %d, ldb, ldv >= n)", kTridiagMax);
+    if (wsb < tssvd_sym_eig_workspace(n)) fail(TSSVD_ENOMEM, "sym_eig_ql workspace too small");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    double* vecs = static_cast<double*>(ws);
+    int* info = reinterpret_cast<int*>(vecs + (size_t)n * n);
+    CU(launch_tridiag_eig(B, (int)ldb, (int)n, kEps, vecs, (int)n, lambda, info, s));
+    copy2d(vecs, n, Vt, ldv, n, (int)n, s);  // eigenvector j (contiguous) -> row j of Vt
+    CU(cudaGetLastError());
+    int h[7];
+    CU(cudaMemcpyAsync(h, info, 28, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    if (iterations) *iterations = h[0];
+    if (h[6]) fail(TSSVD_ENONFINITE, "sym_eig_ql: non-finite input");
+    if (!h[1]) fail(TSSVD_ENOCONV, "sym_eig_ql: QL did not deflate within 30 iterations");
   });
 }
 

@@ -74,6 +74,13 @@ cudaError_t launch_jacobi_svd(const double* cols, int ldc, int N, int ldot, doub
                               int max_sweeps, double* out, int ldout, double* vals, int* info,
                               cudaStream_t s);
 
+// ---- tridiagonal QL eigensolver (tridiag_eig.cu): Alg. 4 step 8 on Z = Y^* Y ~ I ----
+// Same contract and info layout as launch_jacobi_eig (info[0] = QL iterations, info[5] =
+// rotations); n <= kTridiagMax (one CTA, the matrix in shared memory).
+constexpr int kTridiagMax = 160;
+cudaError_t launch_tridiag_eig(const double* B, int ldb, int n, double trunc, double* vecs, int ldv, double* vals,
+                               int* info, cudaStream_t s);
+
 // ---- wide cores, 256 < n <= 2048 (jacobi_wide.cu): cooperative multi-CTA solvers ----
 // Same contracts as launch_jacobi_eig / launch_jacobi_svd, plus a device workspace of
 // jacobi_wide_workspace(n, L) doubles (n = order / max(N, dot), L = rows per column).

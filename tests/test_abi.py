@@ -59,6 +59,10 @@ def test_workspace_queries_and_validation_without_gpu():
     assert h.lowrank_workspace_size(None, 100, 50, 50, ctypes.byref(o), ctypes.byref(nb)) == 1
     out = ctypes.c_void_p()
     assert h.tssvd_comm_wrap_nccl(None, ctypes.byref(out)) == 1 and not out.value  # NULL comm: EINVAL
+    # the QL eigensolver's limits are argument errors, checked before any device work
+    assert h.tssvd_sym_eig_ql(None, 161, None, 161, None, None, 161, None, None, 0) == 1
+    assert b"1 <= n <= 160" in h.tssvd_last_error()
+    assert h.tssvd_sym_eig_ql(None, 10, None, 9, None, None, 10, None, None, 0) == 1
 
 
 def test_no_cpu_fallback_in_product_package():
