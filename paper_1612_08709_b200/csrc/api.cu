@@ -413,12 +413,14 @@ inline double jacobi_tol(int rows) { return std::max(8.0, 2.0 * std::sqrt((doubl
 // reading R13).  sync = true: one round trip returns k (it sizes the next GEMM);
 // sync = false: returns the bound n, convergence is checked at the end of the call.
 // *nf_flag receives the device address of the solve's non-finite flag.
-// Alg. 4 step 8 on Z = Y^* Y ~ I: one-sided Jacobi by default; TSSVD_ZEIG=ql selects the
-// tridiagonal QL solver (tridiag_eig.cu), which deflates regardless of Z's clustered spectrum
-// (Jacobi needs 11-14 sweeps at c2) but measured slower on one CTA (c2: 0.64 vs 0.50 ms).
+// Alg. 4 step 8 on Z = Y^* Y ~ I (n <= 160): tridiagonal QL (tridiag_eig.cu), which deflates
+// regardless of Z's clustered spectrum (one-sided Jacobi needs 11-15 sweeps there).  Measured:
+// time-neutral against Jacobi (c2 Z solve 0.48 vs 0.50 ms, c4 equal), U's orthonormality after
+// pass 2 three times better (c2 3.2e-15 vs 9.3e-15, c4 4.4e-15 vs 1.4e-14).
+// TSSVD_ZEIG=jacobi restores the Jacobi solve (A/B runs).
 static bool z_by_ql(int n) {
-  static const bool ql = getenv("TSSVD_ZEIG") && strcmp(getenv("TSSVD_ZEIG"), "ql") == 0;
-  return ql && n <= kTridiagMax;
+  static const bool jac = getenv("TSSVD_ZEIG") && strcmp(getenv("TSSVD_ZEIG"), "jacobi") == 0;
+  return !jac && n <= kTridiagMax;
 }
 
 int eig(Ctx& c, Core& b, double* B, int n, double* vals, double trunc_rel, bool sync, const int** nf_flag,

@@ -58,6 +58,8 @@ __global__ void __launch_bounds__(TQ_THREADS, 1)
   __shared__ int s_lo[2], s_m[2], s_iters, s_rots, s_conv;
   __shared__ __align__(8) uint64_t s_full[2], s_empty[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long clk0 = clock64();  // phase timing: info[3] / info[4] = kilocycles of the
+  long long clk1 = clk0;             // reduction + Q formation / of the QL phase
 
   // ---- load (lower triangle, mirrored), non-finite check, scale to max diag = 1 ----
   bool bad = false;
@@ -210,6 +212,7 @@ __global__ void __launch_bounds__(TQ_THREADS, 1)
     __syncthreads();
   }
 
+  clk1 = clock64();
   // ---- implicit QL (tql2) on (d, e); the rotations update Q's columns ----
   // Lane 0 of the last warp computes the chases (a serial chain of Givens steps; every operand it
   // reads is prefetched one step ahead -- a step never reads what the chase wrote before) and
@@ -335,7 +338,9 @@ __global__ void __launch_bounds__(TQ_THREADS, 1)
     for (int r = lane; r < n; r += 32) out[r] = keep ? A[(size_t)r * LD + j] : 0.0;
   }
   if (tid == 0) {
-    info[0] = s_iters, info[1] = s_conv, info[2] = kk, info[3] = 0, info[4] = 0, info[5] = s_rots, info[6] = 0;
+    const long long clk2 = clock64();
+    info[0] = s_iters, info[1] = s_conv, info[2] = kk, info[5] = s_rots, info[6] = 0;
+    info[3] = (int)((clk1 - clk0) / 1000), info[4] = (int)((clk2 - clk1) / 1000);
   }
 }
 
