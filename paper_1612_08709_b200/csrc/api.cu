@@ -418,9 +418,11 @@ inline double jacobi_tol(int rows) { return std::max(8.0, 2.0 * std::sqrt((doubl
 // time-neutral against Jacobi (c2 Z solve 0.48 vs 0.50 ms, c4 equal), U's orthonormality after
 // pass 2 three times better (c2 3.2e-15 vs 9.3e-15, c4 4.4e-15 vs 1.4e-14).
 // TSSVD_ZEIG=jacobi restores the Jacobi solve (A/B runs).
+// Below 48 columns Jacobi is faster (c3's 25-column Z: ~50 us in 2-5 sweeps vs 135 us for QL,
+// whose serial chase and reduction barriers do not shrink with n as fast).
 static bool z_by_ql(int n) {
   static const bool jac = getenv("TSSVD_ZEIG") && strcmp(getenv("TSSVD_ZEIG"), "jacobi") == 0;
-  return !jac && n <= kTridiagMax;
+  return !jac && n >= 48 && n <= kTridiagMax;
 }
 
 int eig(Ctx& c, Core& b, double* B, int n, double* vals, double trunc_rel, bool sync, const int** nf_flag,

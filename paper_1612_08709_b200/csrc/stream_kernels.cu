@@ -557,14 +557,14 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
     const int kc_here = q.chunk;
     if constexpr (SK)
       if (s == 0 || kc_here == 0) partial = kc_here != 0;
-    // k-steps holding real columns (KCT: all of them, the zero-filled ones included)
-    const int nks = KCT > 0 ? KCT / 4 : min(KC / 4, (k - kc_here * KC + 3) / 4);
+    // k-steps holding real columns (stream-K with KCT: all of them, the zero-filled ones included)
+    const int nks = SK && KCT > 0 ? KCT / 4 : min(KC / 4, (k - kc_here * KC + 3) / 4);
     // (software-pipelining the fragment loads, as gemm_tn does, measured slower
     // here: 7.9 -> 9.0 ms per c3 alpha pass.)  SK: the fragments of a k-step are loaded
     // before its first DMMA (c3 alpha 7.2 -> 6.9 ms); the same source order made the
     // row-tile passes slower (c2 A V~ 1.06 -> 1.18 ms), so they keep the per-column-block
     // loads (measured r2, tools/nn_bench.py).
-    if constexpr (!SK) for (int kk = 0; kk < nks; ++kk) {
+    auto row_tile_step = [&](int kk) {
       double a[MI];
 #pragma unroll
       for (int i = 0; i < MI; ++i) a[i] = xs[i * 8 * KC + kk * 4];
@@ -582,8 +582,14 @@ __global__ void __launch_bounds__(32 * (NN_CW + 1)) gemm_nn_kernel(
           for (int i = 0; i < MI; ++i) ex[i][x] = fma(a[i], mv, ex[i][x]);
         }
       }
-    }
-    else
+    };
+    if constexpr (!SK && KCT > 0) {  // constant chunk: unrolled, the last chunk's padding skipped
+#pragma unroll
+      for (int kk = 0; kk < KCT / 4; ++kk)
+        if (kk < nks) row_tile_step(kk);
+    } else if constexpr (!SK) {
+      for (int kk = 0; kk < nks; ++kk) row_tile_step(kk);
+    } else
 #pragma unroll
     for (int kk = 0; kk < nks; ++kk) {
       double a[MI], bfr[NIW], mv[XR > 0 ? XR : 1];
@@ -866,9 +872,12 @@ template <int MI, int NIW, int WC, int XR>
 static cudaError_t nn_go(const NnPlan& p, const CUtensorMap& tx, const CUtensorMap& tm, int64_t m,
                          int k, int c, double* Y, int64_t ldy, double* norm_part, double* sk_rec,
                          cudaStream_t s) {
-  // stream-K with the planner's usual K chunks as compile-time constants (TSSVD_NN_KCT=0: runtime KC)
+  // the planner's usual K chunks as compile-time constants (stream-K: 20, 28; row tiles: 28, 52;
+  // TSSVD_NN_KCT=0: runtime KC, A/B runs)
   static const bool kct = !getenv("TSSVD_NN_KCT") || atoi(getenv("TSSVD_NN_KCT")) != 0;
-  auto kern = !sk_rec ? gemm_nn_kernel<MI, NIW, WC, XR, false>
+  auto kern = !sk_rec ? (kct && p.KC == 28   ? gemm_nn_kernel<MI, NIW, WC, XR, false, 28>
+                         : kct && p.KC == 52 ? gemm_nn_kernel<MI, NIW, WC, XR, false, 52>
+                                             : gemm_nn_kernel<MI, NIW, WC, XR, false>)
               : kct && p.KC == 20 ? gemm_nn_kernel<MI, NIW, WC, XR, true, 20>
               : kct && p.KC == 28 ? gemm_nn_kernel<MI, NIW, WC, XR, true, 28>
                                   : gemm_nn_kernel<MI, NIW, WC, XR, true>;
