@@ -872,12 +872,13 @@ template <int MI, int NIW, int WC, int XR>
 static cudaError_t nn_go(const NnPlan& p, const CUtensorMap& tx, const CUtensorMap& tm, int64_t m,
                          int k, int c, double* Y, int64_t ldy, double* norm_part, double* sk_rec,
                          cudaStream_t s) {
-  // the planner's usual K chunks as compile-time constants (stream-K: 20, 28; row tiles: 28, 52;
+  // the planner's usual K chunks as compile-time constants (stream-K: 20, 28; row tiles: 52;
   // TSSVD_NN_KCT=0: runtime KC, A/B runs)
   static const bool kct = !getenv("TSSVD_NN_KCT") || atoi(getenv("TSSVD_NN_KCT")) != 0;
-  auto kern = !sk_rec ? (kct && p.KC == 28   ? gemm_nn_kernel<MI, NIW, WC, XR, false, 28>
-                         : kct && p.KC == 52 ? gemm_nn_kernel<MI, NIW, WC, XR, false, 52>
-                                             : gemm_nn_kernel<MI, NIW, WC, XR, false>)
+  // (row tiles with KC = 28 measured 7% slower as a constant -- c2's 55-column passes: 0.471 ->
+  // 0.506 ms -- and KC = 52 2% faster: c2 A V~ 1.007 -> 0.988 ms, c4 14.21 -> 13.89 ms)
+  auto kern = !sk_rec ? (kct && p.KC == 52 ? gemm_nn_kernel<MI, NIW, WC, XR, false, 52>
+                                           : gemm_nn_kernel<MI, NIW, WC, XR, false>)
               : kct && p.KC == 20 ? gemm_nn_kernel<MI, NIW, WC, XR, true, 20>
               : kct && p.KC == 28 ? gemm_nn_kernel<MI, NIW, WC, XR, true, 28>
                                   : gemm_nn_kernel<MI, NIW, WC, XR, true>;
