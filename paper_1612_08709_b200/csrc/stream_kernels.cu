@@ -125,7 +125,11 @@ __device__ __forceinline__ void ring_init(Ring r, int nst, int consumers) {
 // of a run share their row fragment.  Both operands are columns of the same
 // row block: the fragment of column block c at k-step kk is Xs[kk*4+t][c*8+g]
 // in the A (= X^T) and the B role alike.
+#ifdef TSSVD_SYRK_KR
+static constexpr int SYRK_KR = TSSVD_SYRK_KR;  // A/B builds (build.py -D TSSVD_SYRK_KR=64)
+#else
 static constexpr int SYRK_KR = 32;
+#endif
 static constexpr int SYRK_TPW = 11;
 // CTAs per SM: runs of <= 6 tiles fit 64 registers (two CTAs per SM), longer
 // runs need up to 128 (one CTA per SM)
