@@ -378,13 +378,18 @@ def run_ours(args, rank, world, local_rank):
     clocks = NvmlClocks(local_rank) if os.environ.get("BENCH_CLOCKS") == "nvml" else Clocks(local_rank)
     if not args.no_clocks:
         clocks.start()
+    # pass timing on already in the warm-up: it is part of a call's CUDA-graph key, and the
+    # warm-up must capture the graphs the timed steps replay (the outputs of consecutive calls
+    # alternate between two buffer sets: >= 2 warm-up steps capture both).  Switching it on at
+    # the timed region made the first timed steps capture + instantiate their graphs inside the
+    # timed region (c3: up to 10 ms/step of GPU idle in some runs).
+    _lib.set_pass_timing(True)
     for _ in range(args.warmup):
-        step()
+        out = step()
     st = _lib.last_stats()
     launches = st["kernel_launches"]
     barrier()
     clocks.mark_begin()
-    _lib.set_pass_timing(True)
     pass_ms = {}
     pass_flops = {}
     pass_kinds, pass_bytes = [], []
