@@ -82,6 +82,19 @@ class Comm:
 
 
 _ws_cache: dict = {}
+_ws_size_cache: dict = {}
+
+
+def _ws_size(fn, cptr, dims, opts) -> int:
+    """The library's workspace size for these arguments, remembered per (entry point, comm,
+    shape, options): the query runs the host planner, ~40 us a call."""
+    key = (fn.__name__, cptr, dims, bytes(opts))
+    v = _ws_size_cache.get(key)
+    if v is None:
+        nbytes = ctypes.c_size_t()
+        check(fn(cptr, *dims, ctypes.byref(opts), ctypes.byref(nbytes)))
+        v = _ws_size_cache[key] = nbytes.value
+    return v
 
 
 def _workspace(nbytes: int, device: torch.device) -> torch.Tensor:
@@ -113,8 +126,7 @@ def tssvd(A: torch.Tensor, wp: float = 1e-11, passes: int = 2, comm: Comm | None
         torch.device("cuda", torch.cuda.current_device()) if host else A.device)
     opts = default_opts(wp, passes, max_sweeps, host_io=host)
     cptr = comm.ptr if comm else None
-    nbytes = ctypes.c_size_t()
-    check(lib().tssvd_workspace_size(cptr, m, n, ctypes.byref(opts), ctypes.byref(nbytes)))
+    nbytes = ctypes.c_size_t(_ws_size(lib().tssvd_workspace_size, cptr, (m, n), opts))
     ws = _workspace(nbytes.value, dev)
     pin = host and torch.cuda.is_available()
     packed = host and U is None  # host_io: U comes back packed (ld (r+1)&~1), one D2H copy
@@ -164,9 +176,8 @@ def lowrank_svd(A: torch.Tensor, Omega: torch.Tensor, iters: int, k: int | None 
         raise ValueError("out_of_core needs A in host memory")
     opts = default_opts(wp, 2, max_sweeps, host_io=2 if out_of_core else host)
     cptr = comm.ptr if comm else None
-    nbytes = ctypes.c_size_t()
     wsf = lib().lowrank_lu_workspace_size if tracking == "lu" else lib().lowrank_workspace_size
-    check(wsf(cptr, m, n, l, ctypes.byref(opts), ctypes.byref(nbytes)))
+    nbytes = ctypes.c_size_t(_ws_size(wsf, cptr, (m, n, l), opts))
     ws = _workspace(nbytes.value, dev)
     pin = host and torch.cuda.is_available()
     kk = max(k, 1)
@@ -208,8 +219,7 @@ def tsqr_svd(A: torch.Tensor, phases: torch.Tensor, perms: torch.Tensor, wp: flo
     phases, perms = _mixing(phases, perms, A.device)
     opts = default_opts(wp, passes, max_sweeps)
     cptr = comm.ptr if comm else None
-    nbytes = ctypes.c_size_t()
-    check(lib().tsqr_svd_workspace_size(cptr, m, n, ctypes.byref(opts), ctypes.byref(nbytes)))
+    nbytes = ctypes.c_size_t(_ws_size(lib().tsqr_svd_workspace_size, cptr, (m, n), opts))
     ws = _workspace(nbytes.value, A.device)
     U = A if inplace else torch.empty((m, n + (n & 1)), dtype=torch.float64, device=A.device)
     sigma = torch.empty(n, dtype=torch.float64, device=A.device)
@@ -242,8 +252,7 @@ def lowrank_svd_tsqr(A: torch.Tensor, Omega: torch.Tensor, iters: int, phases: t
         raise ValueError("phases / perms must be l x l tables")
     opts = default_opts(wp, 2, max_sweeps)
     cptr = comm.ptr if comm else None
-    nbytes = ctypes.c_size_t()
-    check(lib().lowrank_tsqr_workspace_size(cptr, m, n, l, ctypes.byref(opts), ctypes.byref(nbytes)))
+    nbytes = ctypes.c_size_t(_ws_size(lib().lowrank_tsqr_workspace_size, cptr, (m, n, l), opts))
     ws = _workspace(nbytes.value, A.device)
     kk = max(k, 1)
     ldu = kk + (kk & 1)
