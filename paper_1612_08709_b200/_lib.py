@@ -153,9 +153,18 @@ def default_opts(wp: float = 1e-11, passes: int = 2, max_sweeps: int = 60, host_
     return o
 
 
-def last_stats() -> dict:
+def raw_stats() -> "TssvdStats":
+    """The last call's stats as the raw struct (a few us; decode later with decode_stats)."""
     s = TssvdStats()
     check(lib().tssvd_last_stats(ctypes.byref(s)))
+    return s
+
+
+def last_stats() -> dict:
+    return decode_stats(raw_stats())
+
+
+def decode_stats(s: "TssvdStats") -> dict:
     passes = [dict(kind=PASS_KINDS.get(s.pass_kind[i], s.pass_kind[i]), ms=s.pass_ms[i],
                    flops=s.pass_flops[i], bytes=s.pass_bytes[i]) for i in range(s.n_pass)]
     return dict(kernel_launches=s.kernel_launches, a_passes=s.a_passes,
