@@ -125,13 +125,14 @@ __device__ __forceinline__ void ring_init(Ring r, int nst, int consumers) {
 // of a run share their row fragment.  Both operands are columns of the same
 // row block: the fragment of column block c at k-step kk is Xs[kk*4+t][c*8+g]
 // in the A (= X^T) and the B role alike.
-// rows per pipeline stage: 64 (16 k-steps between stage hand-offs) measured 1.4-2.5% faster than
-// 32 at w = 92..200 and equal at w = 25..55 (c2 Gram 0.773 -> 0.762 ms, c4 10.84 -> 10.65 ms;
-// profiles/r02s2_gram_kr64_ab.txt); A/B builds: build.py -D TSSVD_SYRK_KR=32
+// rows per pipeline stage.  64 rows measured 1.4-2.5% faster at w = 92..200 (c2 Gram 0.773 ->
+// 0.762 ms, c4 10.84 -> 10.65 ms; profiles/r02s2_gram_kr64_ab.txt) but two 64-row stages of a
+// 256-column box exceed the 227 KB of shared memory (w = 256 failed to launch), so the default
+// stays 32; A/B builds: build.py -D TSSVD_SYRK_KR=64
 #ifdef TSSVD_SYRK_KR
 static constexpr int SYRK_KR = TSSVD_SYRK_KR;
 #else
-static constexpr int SYRK_KR = 64;
+static constexpr int SYRK_KR = 32;
 #endif
 static constexpr int SYRK_TPW = 11;
 // CTAs per SM: runs of <= 6 tiles fit 64 registers (two CTAs per SM), longer
