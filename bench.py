@@ -6,8 +6,9 @@ A "step" is one whole call of the hot path on a BASELINE.json config, row-sharde
 over N GPUs (strong scaling: the matrix is fixed).  Default: configs[2] (c3:
 200,000 x 20,000 FP64, 32 GB, Alg. 8 randomized low-rank SVD, k=20 l=25 i=2) --
 BASELINE's metric names no config, so the N=1 line runs the largest config that
-fits one GPU's HBM (c5, 160 GB, needs the host to hold A: see tests for the
-on-device-built c5 run); `--config c2` / `c4` run Alg. 4 on configs[1] / [3].
+BASELINE lists for 1 GPU; `--config c2` / `c4` run Alg. 4 on configs[1] / [3];
+`--config c5` (configs[4], 160 GB, listed for 2/4/8 GPUs: A does not fit the host)
+builds each rank's rows of A on its device (same recipe, torch's device generator).
 `value` = A-stream throughput: algorithmic bytes of A streamed by the step's
 passes over A (2 for Alg. 4: the Gram pass and the A V~ pass; 2i+2 for Alg. 8)
 divided by the step time, summed over GPUs (whole job).
@@ -315,10 +316,49 @@ def config_obj(args, cfg, world):
          "m": cfg["m"], "n": cfg["n"], "rows_per_gpu": -(-cfg["m"] // world),
          "working_precision": cfg.get("wp", args.wp), "parallelism": f"row-shard x{world}",
          "l2": "A is larger than L2 (126 MB) on every rank; no flush needed"}
+    if args.config in DEVICE_BUILT and args.impl == "ours":
+        c["inputs"] = ("A and Omega built on each rank's device by torch's generator (the synth "
+                       "recipe's distribution, not its bytes; A does not fit the host)")
     return c
 
 
 # ------------------------------------------------------------ ours -------
+DEVICE_BUILT = ("c5",)  # A too large for the host: built on the device (inputs only, no method)
+
+
+def device_lowrank_inputs(cfg, r0, r1, world, rank, dev):
+    """Rows [r0, r1) of A = U_r diag(sigma) V_r^T + noise G / sqrt(n) and Omega, built on `dev`
+    with torch's device generator (the synth recipe's distribution, other bytes: there is no
+    oracle at this size).  V_r, sigma and Omega are identical on every rank (common seed); the
+    rank's block of U_r is Q_p / sqrt(P) with Q_p the QR factor of the rank's own Gaussian block,
+    so U_r^T U_r = sum_p Q_p^T Q_p / P = I (orthonormal; Haar for P = 1)."""
+    import math
+
+    import torch
+
+    f64 = torch.float64
+    m_local, n, r = r1 - r0, cfg["n"], cfg["r"]
+    gc_ = torch.Generator(device=dev).manual_seed(cfg["seed"])
+    vr, _ = torch.linalg.qr(torch.randn(n, r, generator=gc_, device=dev, dtype=f64))
+    omega = torch.randn((n, cfg["l"]), generator=gc_, device=dev, dtype=f64)
+    sigma = torch.from_numpy(synth.spectrum(cfg["spec"][0], r)).to(dev)
+    b = sigma[:, None] * vr.T  # r x n
+    del vr
+    gr = torch.Generator(device=dev).manual_seed(cfg["seed"] * 1000 + 1 + rank)
+    ur, _ = torch.linalg.qr(torch.randn(m_local, r, generator=gr, device=dev, dtype=f64))
+    ur /= math.sqrt(world)
+    A = torch.empty((m_local, n), device=dev, dtype=f64)
+    step = 2048
+    for i in range(0, m_local, step):
+        j = min(m_local, i + step)
+        torch.randn((j - i, n), generator=gr, device=dev, dtype=f64, out=A[i:j])
+        A[i:j].mul_(cfg["noise"] / math.sqrt(n)).addmm_(ur[i:j], b)
+    del ur, b
+    if dev.type == "cuda":
+        torch.cuda.synchronize(dev)
+    return A, omega
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -331,20 +371,27 @@ def run_ours(args, rank, world, local_rank):
     comm = tk.Comm(device=local_rank) if world > 1 else None
     cfg = synth.CONFIGS[args.config]
     r0, r1 = tk.shard_rows(cfg["m"], world, rank)
-    d = synth.config_inputs(args.config, rows=(r0, r1))
-    # the pinned copy is the only host A kept (the e2e leg's input): the generator's array is
-    # released before any timing (c3: 32 GB), and the host gets a moment to settle after the
-    # large allocations -- first c3 runs on a fresh box showed 10 ms/step of host-side GPU idle
-    a_host = torch.from_numpy(d.pop("A")).pin_memory()
-    A = a_host.to(dev)
+    lowrank = cfg["kind"] == "lowrank"
+    device_built = args.config in DEVICE_BUILT
+    if device_built:
+        if args.method != "gram":
+            raise SystemExit(f"--config {args.config}: device-built inputs run the Gram-based method only")
+        A, Om = device_lowrank_inputs(cfg, r0, r1, world, rank, dev)
+        a_host = om_host = None
+    else:
+        d = synth.config_inputs(args.config, rows=(r0, r1))
+        # the pinned copy is the only host A kept (the e2e leg's input): the generator's array is
+        # released before any timing (c3: 32 GB), and the host gets a moment to settle after the
+        # large allocations -- first c3 runs on a fresh box showed 10 ms/step of host-side GPU idle
+        a_host = torch.from_numpy(d.pop("A")).pin_memory()
+        A = a_host.to(dev)
+        if lowrank:
+            om_host = torch.from_numpy(d["Omega"]).pin_memory()
+            Om = om_host.to(dev)
     gc.collect()
     torch.cuda.synchronize()
     time.sleep(1.0)
     m_local, n = A.shape
-    lowrank = cfg["kind"] == "lowrank"
-    if lowrank:
-        om_host = torch.from_numpy(d["Omega"]).pin_memory()
-        Om = om_host.to(dev)
     U = torch.empty_like(A) if not lowrank else None
 
     wp = cfg.get("wp", args.wp)  # the paper workloads fix their own (reading Q1)
@@ -425,6 +472,10 @@ def run_ours(args, rank, world, local_rank):
     if method == "tsqr":
         e2e = {"value": None, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                "unavailable": "the TSQR entry points take device pointers only (host_io 0)"}
+    elif device_built:
+        e2e = {"value": None, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+               "unavailable": f"{args.config}'s A ({8 * cfg['m'] * cfg['n'] / 1e9:.0f} GB) does not fit "
+                              "the host: built on the device, no host copy to stream"}
     elif not args.no_e2e:
         ts = []
         ew = max(2, min(args.warmup, 3))  # >= 2: the pinned output blocks of two calls are live

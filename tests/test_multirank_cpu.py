@@ -507,3 +507,29 @@ def test_bench_reference_arm_under_torchrun_two_ranks():
     assert rec["impl"] == "reference" and rec["n_gpus"] == 2 and rec["value"] > 0
     assert rec["cpu_baseline"]["kind"] == "oracle"
     assert rec["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_bench_device_built_inputs_shard_consistently():
+    """bench.py's device-built inputs (c5: A does not fit the host) at a reduced size, on the CPU
+    generator: two ranks' shards stacked have the prescribed spectrum sigma_j = exp(-(j-1)/15)
+    (U_r blocks Q_p / sqrt(P): orthonormal across ranks) above the noise floor, and Omega is the
+    same on every rank."""
+    sys.path.insert(0, ROOT)
+    import bench
+    import synth
+
+    cfg = dict(synth.CONFIGS["c5"])
+    cfg.update(m=3_000, n=400)
+    dev = torch.device("cpu")
+    a0, om0 = bench.device_lowrank_inputs(cfg, 0, 1_500, 2, 0, dev)
+    a1, om1 = bench.device_lowrank_inputs(cfg, 1_500, 3_000, 2, 1, dev)
+    assert torch.equal(om0, om1) and om0.shape == (400, cfg["l"])
+    s = np.linalg.svd(torch.cat([a0, a1]).numpy(), compute_uv=False)
+    want = synth.spectrum("exp15", cfg["r"])
+    # the noise 1e-8 G / sqrt(n) has spectral norm ~1e-8 (sqrt(m / n) + 1) ~ 4e-8
+    assert np.max(np.abs(s[:cfg["r"]] - want)) <= 1e-7
+    assert s[cfg["r"]] <= 1e-7
+    # one rank alone (P = 1): U_r is Haar, same spectrum
+    a, _ = bench.device_lowrank_inputs(cfg, 0, 3_000, 1, 0, dev)
+    s1 = np.linalg.svd(a.numpy(), compute_uv=False)
+    assert np.max(np.abs(s1[:cfg["r"]] - want)) <= 1e-7
