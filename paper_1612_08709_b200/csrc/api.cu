@@ -1116,6 +1116,20 @@ CoreOut lu_core(Ctx& c, void* lws, double* X, int64_t ldx, int64_t rows, int w, 
   step("lu_core:%s:%d", dist ? "sharded" : "local", w);
   const LuWork lw = lu_carve(lws, rows, w);
   const int rank = dd ? c.comm->rank : 0;
+  // no collective between the steps (one rank, or a replicated factor): the whole elimination as
+  // one cooperative kernel, bit-identical to the launch-per-step loop below (TSSVD_LU_FUSED=0
+  // forces the loop, for A/B runs)
+  static const bool fused_ok = !(getenv("TSSVD_LU_FUSED") && strcmp(getenv("TSSVD_LU_FUSED"), "0") == 0);
+  if (!dd && fused_ok) {
+    for (int j = 0; j < w; ++j) step("lu_col:%d", j);
+    const int sl = c.next_slot();
+    step("lu_finish");
+    KL(lu_fused(lw, X, ldx, rows, w, wdev, c.wp, c.slot(sl), s));
+    CoreOut out;
+    out.bound = w;
+    out.slot = sl;
+    return out;
+  }
   KL(lu_init(lw, rows, s));
   for (int j = 0; j < w; ++j) {
     step("lu_col:%d", j);

@@ -127,5 +127,7 @@ cudaError_t lu_decide(const LuWork& lw, const double* Y, int64_t ldy, int w, int
                       int rank, cudaStream_t s);
 cudaError_t lu_update(const LuWork& lw, double* Y, int64_t ldy, int64_t rows, int w, int j, cudaStream_t s);
 cudaError_t lu_finish(const LuWork& lw, double* Y, int64_t ldy, int64_t rows, int w, int* slot, cudaStream_t s);
+cudaError_t lu_fused(const LuWork& lw, double* Y, int64_t ldy, int64_t rows, int w, const int* wdev, double wp,
+                     int* slot, cudaStream_t s);
 
 }  // namespace tsk

@@ -115,3 +115,53 @@ def test_lowrank_lu_c3_full_vs_alg8_gpu():
     for u in (u2, v2):
         g = (u.T @ u).cpu().numpy()
         assert np.max(np.abs(g - np.eye(g.shape[0]))) <= 1e-13
+
+
+_LOOP_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1612_08709_b200 as tk
+d = np.load(sys.argv[2])
+dev = torch.device("cuda", 0)
+u, s, v = tk.lowrank_svd(torch.from_numpy(d["a"]).to(dev), torch.from_numpy(d["om"]).to(dev), int(d["it"]),
+                         k=int(d["k"]), tracking="lu")
+np.savez(sys.argv[3], u=u.cpu().numpy(), s=s.cpu().numpy(), v=v.cpu().numpy())
+"""
+
+
+@pytest.mark.parametrize("case", ["ties", "tall", "collapse"])
+def test_lowrank_lu_fused_equals_step_loop(case, tmp_path):
+    """The one-kernel cooperative elimination (k_lu_fused, the single-rank default) against the
+    launch-per-step loop (TSSVD_LU_FUSED=0, the multi-rank path's kernels) in a fresh process:
+    bit-identical U, sigma, V -- integer matrices (many equal |pivot| candidates: the lowest row
+    must win in both), more rows than co-resident threads (several rows per thread), and a rank
+    collapse (the elimination stops early)."""
+    import subprocess
+    import sys
+
+    rng = np.random.default_rng({"ties": 1, "tall": 2, "collapse": 3}[case])
+    if case == "ties":
+        a = rng.integers(-2, 3, size=(6_000, 200)).astype(np.float64)
+        om = rng.integers(-1, 2, size=(200, 24)).astype(np.float64)
+        it, k = 2, 12
+    elif case == "tall":
+        a = rng.standard_normal((400_000, 64)) @ np.diag(np.logspace(0, -5, 64)) @ \
+            np.linalg.qr(rng.standard_normal((64, 64)))[0]
+        om = rng.standard_normal((64, 20))
+        it, k = 2, 16
+    else:
+        a = rng.standard_normal((5_000, 7)) @ rng.standard_normal((7, 150))
+        om = rng.standard_normal((150, 16))
+        it, k = 3, 10
+    inp, out = tmp_path / "in.npz", tmp_path / "out.npz"
+    np.savez(inp, a=a, om=om, it=it, k=k)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TSSVD_LU_FUSED="0")
+    r = subprocess.run([sys.executable, "-c", _LOOP_SCRIPT, root, str(inp), str(out)], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    ref = np.load(out)
+    u, s, v = tk.lowrank_svd(to_dev(a), to_dev(om), it, k=k, tracking="lu")
+    torch.cuda.synchronize()
+    assert np.array_equal(s.cpu().numpy(), ref["s"])
+    assert np.array_equal(u.cpu().numpy(), ref["u"]) and np.array_equal(v.cpu().numpy(), ref["v"])
