@@ -173,7 +173,14 @@ __global__ void __launch_bounds__(LU_T) k_lu_update(double* Y, int64_t ldy, int6
     } else {
       const double mult = y[j] * inv;
       y[j] = mult;
-      for (int c = j + 1; c < w; ++c) y[c] = fma(-mult, urow[c], y[c]);
+      for (int c0 = j + 1; c0 < w; c0 += LU_CH) {  // chunks of independent loads (as k_lu_fused)
+        double u[LU_CH];
+#pragma unroll
+        for (int k = 0; k < LU_CH; ++k) u[k] = c0 + k < w ? y[c0 + k] : 0.0;
+#pragma unroll
+        for (int k = 0; k < LU_CH; ++k)
+          if (c0 + k < w) y[c0 + k] = fma(-mult, urow[c0 + k], u[k]);
+      }
     }
   }
 }
