@@ -543,6 +543,11 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args, cfg)
 
+    # context only (frac stays against the nominal-clock peak): the FP64 pipe's rate scales with the
+    # SM clock, so under sw_power_cap the attainable peak is peak * sm_mhz / sm_max_mhz
+    if ck and ck.get("sm_mhz") and ck.get("sm_max_mhz") and roof["bound"] == "tensor":
+        roof["frac_at_sampled_clock"] = round(achieved / (peak * ck["sm_mhz"] / ck["sm_max_mhz"]), 4)
+
     if rank == 0:
         line = {"metric": metric_name(cfg, method), "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t, 4),
