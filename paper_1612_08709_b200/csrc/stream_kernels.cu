@@ -115,6 +115,14 @@ __device__ __forceinline__ void ring_init(Ring r, int nst, int consumers) {
   __syncthreads();
 }
 
+// 8-byte shared-memory load by shared-window address (volatile asm: ordered against the mbarrier
+// wait before it and the arrive after it)
+__device__ __forceinline__ double lds_f64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
+  return v;
+}
+
 // ============================================================== SYRK (Gram) ==
 // CTA b owns rows [b*rpc, (b+1)*rpc) (rpc a multiple of KR, so only the last
 // CTA's last box can cross m -- and there TMA zero-fills).  The T = nb(nb+1)/2
@@ -199,22 +207,32 @@ __global__ void __launch_bounds__(512, MINB) syrk_kernel(const __grid_constant__
 #pragma unroll
   for (int k = 0; k < TPW; ++k) acc[k][0] = acc[k][1] = 0.0;
 
+  // Shared-window byte addresses of every tile's column fragment (and of the row fragments where a
+  // block row starts) within stage 0, k-row 0: loop invariants in registers.  A load adds only the
+  // warp-uniform (stage, k-step) offset -- the element-index arithmetic per load (unpack, scale,
+  // add the window base) was ~4 integer instructions in front of every LDS, each DMMA right
+  // behind its own load.
+  const uint32_t lane0 = smem_u32(buf) + (uint32_t)(t * W + g) * 8u;
+  uint32_t ac[TPW], ar[TPW];
+#pragma unroll
+  for (int k = 0; k < TPW; ++k) ac[k] = lane0 + (off[k] & 0xffffu) * 8u, ar[k] = lane0 + (off[k] >> 16) * 8u;
+  const uint32_t kstep_b = (uint32_t)(4 * W) * 8u, stage_b = (uint32_t)stage_d * 8u;
+
   int b = 0;
   uint32_t ph = 0;
   for (int s = 0; s < nsteps; ++s) {
     mbar_wait(ring.full(b), ph);
-    const double* base = buf + b * stage_d + t * W + g;
     if (nt > 0) {
+      uint32_t u = (uint32_t)b * stage_b;
 #pragma unroll
-      for (int kk = 0; kk < SYRK_KR / 4; ++kk) {
-        const double* rp = base + kk * 4 * W;
+      for (int kk = 0; kk < SYRK_KR / 4; ++kk, u += kstep_b) {
         double cf[TPW];
 #pragma unroll
-        for (int k = 0; k < TPW; ++k) cf[k] = rp[off[k] & 0xffffu];
-        double fi = rp[off[0] >> 16];
+        for (int k = 0; k < TPW; ++k) cf[k] = lds_f64(ac[k] + u);
+        double fi = lds_f64(ar[0] + u);
 #pragma unroll
         for (int k = 0; k < TPW; ++k) {
-          if ((newrow >> k) & 1u) fi = rp[off[k] >> 16];  // a new block row starts
+          if ((newrow >> k) & 1u) fi = lds_f64(ar[k] + u);  // a new block row starts
           dmma(acc[k], fi, cf[k]);
         }
       }
