@@ -1,16 +1,13 @@
 #!/bin/bash
-# Fourth session, fourth call: source-level ncu capture of the narrow Gram (w = 55 and w = 100 at
-# m = 2e6) -- what bounds it, since the busiest SMSP's DMMA slots do not (gram_smsp_balance_ab.txt).
+# Fourth session: ncu --set full of the Gram kernel alone (w = 55, 100, 200 at m = 2e6) on the final
+# build; only the text summaries come back (the reports exceed the 64 MiB return limit).
 set -u
 cd ${GRAFT_REPO_ROOT:-.}
-O=gpurun_out/s4d; mkdir -p $O
-CMD="python tools/gram_bench.py --m 2000000 --w 55 100"
-timeout 300 $CMD > $O/plain.log 2>&1 || exit 1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:syrk_kernel -s 2 -c 1 -o $O/prof_w55 python tools/gram_bench.py --m 2000000 --w 55 > $O/ncu55.log 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:syrk_kernel -s 2 -c 1 -o $O/prof_w100 python tools/gram_bench.py --m 2000000 --w 100 > $O/ncu100.log 2>&1
-for t in w55 w100; do
-  python tools/ncu_summary.py $O/prof_$t.ncu-rep > $O/summary_$t.txt 2>&1
-  ncu -i $O/prof_$t.ncu-rep --page source --csv --print-source sass > $O/source_sass_$t.csv 2>/dev/null
-  ncu -i $O/prof_$t.ncu-rep --page details --csv > $O/details_$t.csv 2>/dev/null
+O=gpurun_out/${1:-s4g}; mkdir -p $O
+timeout 300 python tools/gram_bench.py --m 2000000 --w 55 100 200 > $O/plain.log 2>&1 || exit 1
+for w in 55 100 200; do
+  timeout 600 ncu --set full --clock-control none -k regex:syrk_kernel -s 2 -c 1 -o /tmp/prof_w$w python tools/gram_bench.py --m 2000000 --w $w > $O/ncu$w.log 2>&1
+  python tools/ncu_summary.py /tmp/prof_w$w.ncu-rep > $O/summary_w$w.txt 2>&1
+  ncu -i /tmp/prof_w$w.ncu-rep --page details --csv 2>/dev/null | grep -E "Duration|Pipe Fp64|Tensor|DRAM Throughput|Issue Slots Busy|Registers Per|Achieved Occupancy|Bank Conflict|Warp Cycles Per Issued|No Eligible|L1/TEX Hit|Mem Busy|Max Bandwidth" > $O/details_w$w.txt
 done
 echo done > $O/DONE
